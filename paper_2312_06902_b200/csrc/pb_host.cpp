@@ -1,0 +1,1226 @@
+// Host side of the C ABI (include/perseus_b200.h): cost-model fitting,
+// instance packing into flat device layouts, curve tables, LPT ordering,
+// device memory, launches and result access.  Compiled with g++
+// -ffp-contract=off so that pareto/fit/table arithmetic reproduces the
+// reference's libm results bit for bit (SURVEY.md §7 hard part 1).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "g9.hpp"
+#include "pb_internal.h"
+#include "perseus_b200.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+pb_status fail(pb_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ----------------------------------------------------------- owned instance
+
+struct HostInst {
+  int32_t n = 0;
+  std::vector<int32_t> comp_class, edge_tail, edge_head;
+  std::vector<uint8_t> cls_const;
+  std::vector<int32_t> cls_pt_off, pt_freq;
+  std::vector<int64_t> pt_time, pt_energy, cls_trange;
+  std::vector<double> cls_curve;
+  double watts = 75.0;
+  int64_t quantum = 1, tau = 1000;
+  std::vector<int64_t> start;  // empty = min-energy seed
+  int32_t max_steps = 0;
+  // derived by validate()
+  int32_t n_levels = 0;
+  std::vector<int32_t> lvl_off, lvl_comps, in_off, in_dep, out_off, out_dep, snk_dep;
+  std::vector<int32_t> inc_off, inc, ec_tail, ec_head;
+  int64_t t_min_est = 0, t_star_est = 0, est_steps = 0, work = 0;
+};
+
+// Longest path on the node DAG with the given durations (host estimate used
+// only to size output buffers and order work; the device computes its own).
+int64_t host_makespan(const HostInst& h, const std::vector<int64_t>& dur) {
+  std::vector<int64_t> start(h.n, 0);
+  for (int32_t L = 0; L < h.n_levels; ++L)
+    for (int32_t q = h.lvl_off[L]; q < h.lvl_off[L + 1]; ++q) {
+      const int32_t i = h.lvl_comps[q];
+      int64_t m = 0;
+      for (int32_t j = h.in_off[i]; j < h.in_off[i + 1]; ++j) {
+        const int32_t u = h.edge_tail[h.in_dep[j]];
+        if (u < h.n) m = std::max(m, start[u] + dur[u]);
+      }
+      start[i] = m;
+    }
+  int64_t ms = 0;
+  for (int32_t j : h.snk_dep) {
+    const int32_t u = h.edge_tail[j];
+    if (u < h.n) ms = std::max(ms, start[u] + dur[u]);
+  }
+  return ms;
+}
+
+// Validation mirrors the reference's throws; derived arrays are the static
+// device layout (levels, CSRs, edge-centric incidence).
+pb_status validate_and_derive(HostInst& h) {
+  const int32_t n = h.n, ne = static_cast<int32_t>(h.edge_tail.size());
+  const int32_t nc = static_cast<int32_t>(h.cls_const.size());
+  if (n < 1) return fail(PB_ERR_INVALID_ARGUMENT, "dag needs at least one computation");
+  if (h.tau <= 0) return fail(PB_ERR_INVALID_ARGUMENT, "tau must be positive");
+  if (h.quantum <= 0) return fail(PB_ERR_INVALID_ARGUMENT, "quantum must be positive");
+  for (int32_t c = 0; c < nc; ++c) {
+    const int32_t np = h.cls_pt_off[c + 1] - h.cls_pt_off[c];
+    if (np < 1) return fail(PB_ERR_INVALID_ARGUMENT, "profile has no points");
+    if (np > 255) return fail(PB_ERR_INVALID_ARGUMENT, "more than 255 Pareto points in a class");
+    for (int32_t p = h.cls_pt_off[c]; p < h.cls_pt_off[c + 1]; ++p)
+      if (h.pt_time[p] < 0) return fail(PB_ERR_INVALID_ARGUMENT, "durations must be non-negative");
+    if (!h.cls_const[c] && h.cls_trange[2 * c] > h.cls_trange[2 * c + 1])
+      return fail(PB_ERR_INVALID_ARGUMENT, "curve interval is empty");
+  }
+  for (int32_t i = 0; i < n; ++i)
+    if (h.comp_class[i] < 0 || h.comp_class[i] >= nc)
+      return fail(PB_ERR_INVALID_ARGUMENT, "missing profile for a computation class");
+  for (int32_t j = 0; j < ne; ++j) {
+    const int32_t u = h.edge_tail[j], v = h.edge_head[j];
+    if (u < 0 || u > n + 1 || v < 0 || v > n + 1 || u == n + 1 || v == n || u == v)
+      return fail(PB_ERR_INVALID_ARGUMENT, "edge references unknown computation");
+  }
+  if (!h.start.empty()) {
+    if (static_cast<int32_t>(h.start.size()) != n)
+      return fail(PB_ERR_INVALID_ARGUMENT, "durations must cover every computation");
+    for (int64_t t : h.start)
+      if (t < 0) return fail(PB_ERR_INVALID_ARGUMENT, "durations must be non-negative");
+  }
+  // Kahn over the full node set (dag.hpp:64-86) for cycle detection, levels
+  // over computations = longest hop distance from any root.
+  std::vector<int32_t> indeg(n + 2, 0);
+  std::vector<std::vector<int32_t>> succ(n + 2);
+  for (int32_t j = 0; j < ne; ++j) {
+    succ[h.edge_tail[j]].push_back(h.edge_head[j]);
+    ++indeg[h.edge_head[j]];
+  }
+  std::vector<int32_t> order, level(n + 2, 0);
+  order.reserve(n + 2);
+  for (int32_t v = 0; v < n + 2; ++v)
+    if (indeg[v] == 0) order.push_back(v);
+  for (size_t q = 0; q < order.size(); ++q) {
+    const int32_t u = order[q];
+    for (int32_t v : succ[u]) {
+      if (u < n) level[v] = std::max(level[v], level[u] + 1);
+      if (--indeg[v] == 0) order.push_back(v);
+    }
+  }
+  if (static_cast<int32_t>(order.size()) != n + 2)
+    return fail(PB_ERR_INVALID_ARGUMENT, "dependency graph contains a cycle");
+  int32_t L = 0;
+  for (int32_t i = 0; i < n; ++i) L = std::max(L, level[i] + 1);
+  h.n_levels = L;
+  h.lvl_off.assign(L + 1, 0);
+  for (int32_t i = 0; i < n; ++i) ++h.lvl_off[level[i] + 1];
+  for (int32_t l = 0; l < L; ++l) h.lvl_off[l + 1] += h.lvl_off[l];
+  h.lvl_comps.assign(n, 0);
+  {
+    std::vector<int32_t> fill(h.lvl_off.begin(), h.lvl_off.end() - 1);
+    for (int32_t i = 0; i < n; ++i) h.lvl_comps[fill[level[i]]++] = i;
+  }
+  auto csr = [&](bool by_head, std::vector<int32_t>& off, std::vector<int32_t>& idx) {
+    off.assign(n + 1, 0);
+    for (int32_t j = 0; j < ne; ++j) {
+      const int32_t x = by_head ? h.edge_head[j] : h.edge_tail[j];
+      if (x < n) ++off[x + 1];
+    }
+    for (int32_t i = 0; i < n; ++i) off[i + 1] += off[i];
+    idx.assign(off[n], 0);
+    std::vector<int32_t> fill(off.begin(), off.end() - 1);
+    for (int32_t j = 0; j < ne; ++j) {
+      const int32_t x = by_head ? h.edge_head[j] : h.edge_tail[j];
+      if (x < n) idx[fill[x]++] = j;
+    }
+  };
+  csr(true, h.in_off, h.in_dep);
+  csr(false, h.out_off, h.out_dep);
+  h.snk_dep.clear();
+  for (int32_t j = 0; j < ne; ++j)
+    if (h.edge_head[j] == n + 1) h.snk_dep.push_back(j);
+  // edge-centric graph (dag.hpp:209-224) + return arc
+  const int32_t V = 2 * n + 2, E = n + ne + 1;
+  h.ec_tail.assign(E, 0);
+  h.ec_head.assign(E, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    h.ec_tail[i] = 2 * i;
+    h.ec_head[i] = 2 * i + 1;
+  }
+  for (int32_t j = 0; j < ne; ++j) {
+    const int32_t u = h.edge_tail[j], v = h.edge_head[j];
+    h.ec_tail[n + j] = u == n ? 2 * n : 2 * u + 1;
+    h.ec_head[n + j] = v == n + 1 ? 2 * n + 1 : 2 * v;
+  }
+  h.ec_tail[n + ne] = 2 * n + 1;
+  h.ec_head[n + ne] = 2 * n;
+  h.inc_off.assign(V + 1, 0);
+  for (int32_t k = 0; k < E; ++k) {
+    ++h.inc_off[h.ec_tail[k] + 1];
+    ++h.inc_off[h.ec_head[k] + 1];
+  }
+  for (int32_t v = 0; v < V; ++v) h.inc_off[v + 1] += h.inc_off[v];
+  h.inc.assign(h.inc_off[V], 0);
+  {
+    std::vector<int32_t> fill(h.inc_off.begin(), h.inc_off.end() - 1);
+    for (int32_t k = 0; k < E; ++k) {
+      h.inc[fill[h.ec_tail[k]]++] = k << 1;
+      h.inc[fill[h.ec_head[k]]++] = (k << 1) | 1;
+    }
+  }
+  // sizing estimates
+  std::vector<int64_t> fast(n), seed(n);
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t c = h.comp_class[i];
+    fast[i] = h.pt_time[h.cls_pt_off[c]];
+    seed[i] = h.start.empty() ? (h.cls_const[c] ? fast[i] : h.cls_trange[2 * c + 1]) : h.start[i];
+  }
+  h.t_min_est = host_makespan(h, fast);
+  h.t_star_est = host_makespan(h, seed);
+  if (!h.start.empty()) {
+    h.est_steps = std::max<int64_t>(1, h.max_steps);
+  } else {
+    const int64_t gap = std::max<int64_t>(0, h.t_star_est - h.t_min_est);
+    h.est_steps = gap / h.tau + 2;
+    if (h.max_steps > 0) h.est_steps = std::min<int64_t>(h.est_steps, h.max_steps);
+  }
+  h.work = static_cast<int64_t>(E) * h.est_steps;
+  return PB_OK;
+}
+
+// ------------------------------------------------------------------- blobs
+
+struct Blob {
+  std::vector<char> bytes;
+  size_t put(const void* p, size_t n) {
+    const size_t at = (bytes.size() + 255) / 256 * 256;
+    bytes.resize(at + n);
+    if (n && p) std::memcpy(bytes.data() + at, p, n);
+    return at;
+  }
+  template <class T>
+  size_t put(const std::vector<T>& v) {
+    return put(v.data(), v.size() * sizeof(T));
+  }
+};
+
+struct CurveKey {
+  uint64_t a, b, c;
+  int64_t lo, hi;
+  bool operator<(const CurveKey& o) const {
+    return std::tie(a, b, c, lo, hi) < std::tie(o.a, o.b, o.c, o.lo, o.hi);
+  }
+};
+
+uint64_t bits(double d) {
+  uint64_t u;
+  std::memcpy(&u, &d, 8);
+  return u;
+}
+
+struct DeviceRun {
+  int device = -1;
+  char* d_static = nullptr;
+  char* d_out = nullptr;
+  char* d_ws = nullptr;
+  pb::DevInst* d_insts = nullptr;
+  int32_t* d_order = nullptr;
+  int32_t* d_counter = nullptr;
+  pb::RunCounters* d_counters = nullptr;
+  size_t out_bytes = 0;
+  int32_t slots = 0;
+  pb::WsLayout ws{};
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  char* h_out = nullptr;  // pinned
+  void release() {
+    if (device < 0) return;
+    cudaSetDevice(device);
+    cudaFree(d_static);
+    cudaFree(d_out);
+    cudaFree(d_ws);
+    cudaFree(d_insts);
+    cudaFree(d_order);
+    cudaFree(d_counter);
+    cudaFree(d_counters);
+    if (h_out) cudaFreeHost(h_out);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+    *this = DeviceRun{};
+  }
+};
+
+}  // namespace
+
+struct pb_batch {
+  std::vector<HostInst> insts;
+  // packed host-side view (tables kept for host expansion)
+  std::vector<double> tables;
+  std::vector<std::vector<int64_t>> cls_tab;  // per instance per class
+  // outputs (host copies)
+  std::vector<size_t> out_points, out_ids, out_choice, out_summary;
+  std::vector<int32_t> cap_points, cap_ids;
+  std::vector<char> out;  // host results
+  bool have_results = false;
+  DeviceRun run;
+  pb_run_stats stats{};
+  ~pb_batch() { run.release(); }
+};
+
+namespace {
+
+// Packs all instances; returns host blobs and per-instance DevInst with
+// offsets (converted to device pointers once the blob is uploaded).
+struct Packed {
+  Blob stat;
+  std::vector<pb::DevInst> dev;
+  std::vector<std::array<size_t, 32>> offs;
+  size_t out_bytes = 0;
+  int64_t max_n = 1, max_v = 1, max_e = 1;
+  std::vector<int32_t> order;
+};
+
+enum OffIdx {
+  O_CLASS, O_LVLOFF, O_LVL, O_INOFF, O_INDEP, O_OUTOFF, O_OUTDEP, O_SNK, O_DTAIL, O_DHEAD,
+  O_INCOFF, O_INC, O_ECT, O_ECH, O_CCONST, O_CTMIN, O_CTMAX, O_CTAB, O_CPOFF, O_PTIME, O_PENERGY,
+  O_START, O_POINTS, O_IDS, O_CHOICE, O_SUMMARY, O_COUNT
+};
+
+void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, std::vector<int32_t>& cap_ids,
+          double cap_scale) {
+  const size_t N = b->insts.size();
+  // curve tables, deduplicated by (a, b, c, t_min, t_max) bit patterns
+  std::map<CurveKey, int64_t> table_of;
+  b->tables.clear();
+  b->cls_tab.assign(N, {});
+  for (size_t k = 0; k < N; ++k) {
+    const HostInst& h = b->insts[k];
+    const size_t nc = h.cls_const.size();
+    b->cls_tab[k].assign(nc, 0);
+    for (size_t c = 0; c < nc; ++c) {
+      if (h.cls_const[c]) continue;
+      const double a = h.cls_curve[3 * c], bb = h.cls_curve[3 * c + 1], cc = h.cls_curve[3 * c + 2];
+      const int64_t lo = h.cls_trange[2 * c], hi = h.cls_trange[2 * c + 1];
+      const CurveKey key{bits(a), bits(bb), bits(cc), lo, hi};
+      auto it = table_of.find(key);
+      if (it == table_of.end()) {
+        const int64_t at = static_cast<int64_t>(b->tables.size());
+        const int64_t span = hi - lo + 1;
+        if (span > (int64_t{1} << 27)) throw std::length_error("curve interval too long to tabulate");
+        b->tables.resize(b->tables.size() + span);
+        // ExpCurve::eval (costmodel.hpp:47), same expression and libm
+        for (int64_t t = lo; t <= hi; ++t)
+          b->tables[at + (t - lo)] = a * std::exp(bb * static_cast<double>(t)) + cc;
+        it = table_of.emplace(key, at).first;
+      }
+      b->cls_tab[k][c] = it->second;
+    }
+  }
+  const size_t tables_off = P.stat.put(b->tables);
+  P.dev.assign(N, pb::DevInst{});
+  P.offs.assign(N, {});
+  cap_points.assign(N, 0);
+  cap_ids.assign(N, 0);
+  size_t out = 0;
+  auto out_take = [&](size_t bytes) {
+    const size_t at = (out + 255) / 256 * 256;
+    out = at + bytes;
+    return at;
+  };
+  for (size_t k = 0; k < N; ++k) {
+    const HostInst& h = b->insts[k];
+    auto& o = P.offs[k];
+    std::vector<uint8_t> cconst = h.cls_const;
+    std::vector<int64_t> tmin(h.cls_const.size()), tmax(h.cls_const.size());
+    for (size_t c = 0; c < h.cls_const.size(); ++c) {
+      tmin[c] = h.cls_trange[2 * c];
+      tmax[c] = h.cls_trange[2 * c + 1];
+    }
+    o[O_CLASS] = P.stat.put(h.comp_class);
+    o[O_LVLOFF] = P.stat.put(h.lvl_off);
+    o[O_LVL] = P.stat.put(h.lvl_comps);
+    o[O_INOFF] = P.stat.put(h.in_off);
+    o[O_INDEP] = P.stat.put(h.in_dep);
+    o[O_OUTOFF] = P.stat.put(h.out_off);
+    o[O_OUTDEP] = P.stat.put(h.out_dep);
+    o[O_SNK] = P.stat.put(h.snk_dep);
+    o[O_DTAIL] = P.stat.put(h.edge_tail);
+    o[O_DHEAD] = P.stat.put(h.edge_head);
+    o[O_INCOFF] = P.stat.put(h.inc_off);
+    o[O_INC] = P.stat.put(h.inc);
+    o[O_ECT] = P.stat.put(h.ec_tail);
+    o[O_ECH] = P.stat.put(h.ec_head);
+    o[O_CCONST] = P.stat.put(cconst);
+    o[O_CTMIN] = P.stat.put(tmin);
+    o[O_CTMAX] = P.stat.put(tmax);
+    o[O_CTAB] = P.stat.put(b->cls_tab[k]);
+    o[O_CPOFF] = P.stat.put(h.cls_pt_off);
+    o[O_PTIME] = P.stat.put(h.pt_time);
+    o[O_PENERGY] = P.stat.put(h.pt_energy);
+    o[O_START] = h.start.empty() ? SIZE_MAX : P.stat.put(h.start);
+    const int64_t est = static_cast<int64_t>(static_cast<double>(h.est_steps) * cap_scale);
+    cap_points[k] = static_cast<int32_t>(std::min<int64_t>(est + 8, INT32_MAX / 2));
+    cap_ids[k] = static_cast<int32_t>(std::min<int64_t>(est * 8 + 2 * int64_t{h.n} + 64, INT32_MAX / 2));
+    o[O_POINTS] = out_take(sizeof(pb_point) * cap_points[k]);
+    o[O_IDS] = out_take(sizeof(int32_t) * cap_ids[k]);
+    o[O_CHOICE] = out_take(cap_ids[k]);
+    o[O_SUMMARY] = out_take(sizeof(pb_frontier_summary));
+    pb::DevInst& d = P.dev[k];
+    d.n = h.n;
+    d.ne = static_cast<int32_t>(h.edge_tail.size());
+    d.n_levels = h.n_levels;
+    d.mode = h.start.empty() ? pb::kModeDiscover : pb::kModeGetNext;
+    d.max_steps = h.start.empty() ? h.max_steps : (h.max_steps == 0 ? 1 : h.max_steps);
+    d.cap_points = cap_points[k];
+    d.cap_ids = cap_ids[k];
+    d.tau = h.tau;
+    d.watts = h.watts;
+    d.quantum = h.quantum;
+    d.n_snk = static_cast<int32_t>(h.snk_dep.size());
+    P.max_n = std::max<int64_t>(P.max_n, h.n);
+    P.max_v = std::max<int64_t>(P.max_v, 2 * int64_t{h.n} + 2);
+    P.max_e = std::max<int64_t>(P.max_e, h.n + static_cast<int64_t>(h.edge_tail.size()) + 1);
+  }
+  P.out_bytes = out;
+  (void)tables_off;
+  // LPT: largest estimated work first
+  P.order.resize(N);
+  std::iota(P.order.begin(), P.order.end(), 0);
+  std::stable_sort(P.order.begin(), P.order.end(), [&](int32_t x, int32_t y) {
+    return b->insts[x].work > b->insts[y].work;
+  });
+  b->cap_points = cap_points;
+  b->cap_ids = cap_ids;
+  b->out_points.assign(N, 0);
+  b->out_ids.assign(N, 0);
+  b->out_choice.assign(N, 0);
+  b->out_summary.assign(N, 0);
+  for (size_t k = 0; k < N; ++k) {
+    b->out_points[k] = P.offs[k][O_POINTS];
+    b->out_ids[k] = P.offs[k][O_IDS];
+    b->out_choice[k] = P.offs[k][O_CHOICE];
+    b->out_summary[k] = P.offs[k][O_SUMMARY];
+  }
+}
+
+template <class T>
+T* dptr(char* base, size_t off) {
+  return off == SIZE_MAX ? nullptr : reinterpret_cast<T*>(base + off);
+}
+
+void bind_device(Packed& P, char* d_static, char* d_out, size_t tables_off) {
+  for (size_t k = 0; k < P.dev.size(); ++k) {
+    auto& o = P.offs[k];
+    pb::DevInst& d = P.dev[k];
+    d.comp_class = dptr<int32_t>(d_static, o[O_CLASS]);
+    d.lvl_off = dptr<int32_t>(d_static, o[O_LVLOFF]);
+    d.lvl_comps = dptr<int32_t>(d_static, o[O_LVL]);
+    d.in_off = dptr<int32_t>(d_static, o[O_INOFF]);
+    d.in_dep = dptr<int32_t>(d_static, o[O_INDEP]);
+    d.out_off = dptr<int32_t>(d_static, o[O_OUTOFF]);
+    d.out_dep = dptr<int32_t>(d_static, o[O_OUTDEP]);
+    d.snk_dep = dptr<int32_t>(d_static, o[O_SNK]);
+    d.dep_tail = dptr<int32_t>(d_static, o[O_DTAIL]);
+    d.dep_head = dptr<int32_t>(d_static, o[O_DHEAD]);
+    d.inc_off = dptr<int32_t>(d_static, o[O_INCOFF]);
+    d.inc = dptr<int32_t>(d_static, o[O_INC]);
+    d.ec_tail = dptr<int32_t>(d_static, o[O_ECT]);
+    d.ec_head = dptr<int32_t>(d_static, o[O_ECH]);
+    d.cls_const = dptr<uint8_t>(d_static, o[O_CCONST]);
+    d.cls_tmin = dptr<int64_t>(d_static, o[O_CTMIN]);
+    d.cls_tmax = dptr<int64_t>(d_static, o[O_CTMAX]);
+    d.cls_tab = dptr<int64_t>(d_static, o[O_CTAB]);
+    d.cls_pt_off = dptr<int32_t>(d_static, o[O_CPOFF]);
+    d.pt_time = dptr<int64_t>(d_static, o[O_PTIME]);
+    d.pt_energy = dptr<int64_t>(d_static, o[O_PENERGY]);
+    d.tables = dptr<double>(d_static, tables_off);
+    d.start_planned_t = dptr<int64_t>(d_static, o[O_START]);
+    d.points = dptr<pb_point>(d_out, o[O_POINTS]);
+    d.ids = dptr<int32_t>(d_out, o[O_IDS]);
+    d.choice = dptr<uint8_t>(d_out, o[O_CHOICE]);
+    d.summary = dptr<pb_frontier_summary>(d_out, o[O_SUMMARY]);
+  }
+}
+
+int32_t device_slots(int device, int64_t n_inst) {
+  int sms = 0;
+  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+  const int per_sm = std::max(1, pb::walk_slots_per_sm());
+  return static_cast<int32_t>(std::min<int64_t>(n_inst, int64_t{sms} * per_sm));
+}
+
+pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
+  b->run.release();
+  b->have_results = false;
+  const size_t N = b->insts.size();
+  if (N == 0) return PB_OK;
+  DeviceRun& R = b->run;
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  R.device = device;
+  Packed P;
+  std::vector<int32_t> capp, capi;
+  pack(b, P, capp, capi, cap_scale);
+  const size_t tables_off = 0;  // tables are the first section of the blob
+  ck(cudaStreamCreateWithFlags(&R.stream, cudaStreamNonBlocking), "stream");
+  ck(cudaEventCreate(&R.ev0), "event");
+  ck(cudaEventCreate(&R.ev1), "event");
+  cudaEvent_t h0, h1;
+  ck(cudaEventCreate(&h0), "event");
+  ck(cudaEventCreate(&h1), "event");
+  ck(cudaMalloc(&R.d_static, std::max<size_t>(P.stat.bytes.size(), 256)), "malloc static");
+  R.out_bytes = std::max<size_t>(P.out_bytes, 256);
+  ck(cudaMalloc(&R.d_out, R.out_bytes), "malloc out");
+  ck(cudaMallocHost(&R.h_out, R.out_bytes), "malloc pinned out");
+  bind_device(P, R.d_static, R.d_out, tables_off);
+  R.ws = pb::make_ws_layout(P.max_n, P.max_v, P.max_e);
+  R.slots = device_slots(device, static_cast<int64_t>(N));
+  ck(cudaMalloc(&R.d_ws, static_cast<size_t>(R.ws.stride) * R.slots), "malloc workspace");
+  ck(cudaMalloc(&R.d_insts, sizeof(pb::DevInst) * N), "malloc insts");
+  ck(cudaMalloc(&R.d_order, sizeof(int32_t) * N), "malloc order");
+  ck(cudaMalloc(&R.d_counter, sizeof(int32_t)), "malloc counter");
+  ck(cudaMalloc(&R.d_counters, sizeof(pb::RunCounters)), "malloc counters");
+  ck(cudaEventRecord(h0, R.stream), "record");
+  ck(cudaMemcpyAsync(R.d_static, P.stat.bytes.data(), P.stat.bytes.size(), cudaMemcpyHostToDevice,
+                     R.stream),
+     "H2D static");
+  ck(cudaMemcpyAsync(R.d_insts, P.dev.data(), sizeof(pb::DevInst) * N, cudaMemcpyHostToDevice,
+                     R.stream),
+     "H2D insts");
+  ck(cudaMemcpyAsync(R.d_order, P.order.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice,
+                     R.stream),
+     "H2D order");
+  ck(cudaEventRecord(h1, R.stream), "record");
+  ck(cudaStreamSynchronize(R.stream), "sync");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, h0, h1);
+  cudaEventDestroy(h0);
+  cudaEventDestroy(h1);
+  b->stats = pb_run_stats{};
+  b->stats.h2d_ms = ms;
+  b->stats.h2d_bytes = static_cast<int64_t>(P.stat.bytes.size() + sizeof(pb::DevInst) * N +
+                                            sizeof(int32_t) * N);
+  return PB_OK;
+}
+
+pb_status launch_impl(pb_batch* b, double* kernel_ms) {
+  DeviceRun& R = b->run;
+  const size_t N = b->insts.size();
+  if (N == 0) {
+    if (kernel_ms) *kernel_ms = 0;
+    return PB_OK;
+  }
+  if (R.device < 0) return fail(PB_ERR_LOGIC, "batch not prepared");
+  ck(cudaSetDevice(R.device), "cudaSetDevice");
+  ck(cudaMemsetAsync(R.d_counter, 0, sizeof(int32_t), R.stream), "memset");
+  ck(cudaMemsetAsync(R.d_counters, 0, sizeof(pb::RunCounters), R.stream), "memset");
+  ck(cudaEventRecord(R.ev0, R.stream), "record");
+  const int rc = pb::launch_walks(R.d_insts, static_cast<int32_t>(N), R.d_order, R.d_counter,
+                                  R.d_ws, R.ws, R.slots, R.d_counters, R.stream);
+  if (rc != 0) throw CudaError(std::string("walk launch: ") + cudaGetErrorString(static_cast<cudaError_t>(rc)));
+  ck(cudaEventRecord(R.ev1, R.stream), "record");
+  ck(cudaStreamSynchronize(R.stream), "walk kernel");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, R.ev0, R.ev1);
+  pb::RunCounters rcnt{};
+  ck(cudaMemcpy(&rcnt, R.d_counters, sizeof rcnt, cudaMemcpyDeviceToHost), "D2H counters");
+  b->stats.kernel_ms = ms;
+  b->stats.arc_scans = static_cast<int64_t>(rcnt.arc_scans);
+  b->stats.node_updates = static_cast<int64_t>(rcnt.node_updates);
+  b->stats.rounds = static_cast<int64_t>(rcnt.rounds);
+  b->stats.kernel_launches += 1;
+  if (kernel_ms) *kernel_ms = ms;
+  return PB_OK;
+}
+
+pb_status fetch_impl(pb_batch* b) {
+  DeviceRun& R = b->run;
+  if (b->insts.empty()) {
+    b->have_results = true;
+    return PB_OK;
+  }
+  ck(cudaSetDevice(R.device), "cudaSetDevice");
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  ck(cudaEventRecord(e0, R.stream), "record");
+  ck(cudaMemcpyAsync(R.h_out, R.d_out, R.out_bytes, cudaMemcpyDeviceToHost, R.stream), "D2H out");
+  ck(cudaEventRecord(e1, R.stream), "record");
+  ck(cudaStreamSynchronize(R.stream), "sync");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  b->out.assign(R.h_out, R.h_out + R.out_bytes);
+  b->stats.d2h_ms = ms;
+  b->stats.d2h_bytes = static_cast<int64_t>(R.out_bytes);
+  b->have_results = true;
+  return PB_OK;
+}
+
+const pb_frontier_summary& summary_of(const pb_batch* b, int32_t k) {
+  return *reinterpret_cast<const pb_frontier_summary*>(b->out.data() + b->out_summary[k]);
+}
+
+bool any_log_full(const pb_batch* b) {
+  for (size_t k = 0; k < b->insts.size(); ++k)
+    if (summary_of(b, static_cast<int32_t>(k)).status == pb::kStatusLogFull) return true;
+  return false;
+}
+
+template <class F>
+pb_status guarded(F&& f) {
+  try {
+    return f();
+  } catch (const CudaError& e) {
+    return fail(PB_ERR_CUDA, e.what());
+  } catch (const std::length_error& e) {
+    return fail(PB_ERR_UNSUPPORTED, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(PB_ERR_CUDA, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(PB_ERR_LOGIC, e.what());
+  }
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+
+extern "C" {
+
+const char* pb_last_error(void) { return g_last_error.c_str(); }
+const char* pb_version(void) { return "perseus-b200 0.1 (sm_100a)"; }
+
+// pareto_filter, costmodel.hpp:70-81
+int32_t pb_pareto_filter(int32_t n, const int32_t* freq, const int64_t* time, const int64_t* energy,
+                         int32_t* out_freq, int64_t* out_time, int64_t* out_energy) {
+  struct P {
+    int32_t f;
+    int64_t t, e;
+  };
+  std::vector<P> pts(n);
+  for (int32_t i = 0; i < n; ++i) pts[i] = {freq[i], time[i], energy[i]};
+  std::stable_sort(pts.begin(), pts.end(), [](const P& x, const P& y) {
+    if (x.t != y.t) return x.t < y.t;
+    if (x.e != y.e) return x.e < y.e;
+    return x.f > y.f;
+  });
+  int32_t k = 0;
+  for (const P& p : pts)
+    if (k == 0 || p.e < out_energy[k - 1]) {
+      out_freq[k] = p.f;
+      out_time[k] = p.t;
+      out_energy[k] = p.e;
+      ++k;
+    }
+  return k;
+}
+
+// fit_exp, costmodel.hpp:87-149: 64-point c grid, log-linear least squares.
+pb_status pb_fit_exp(int32_t n, const int64_t* time, const int64_t* energy, double* out) {
+  if (n < 2) return fail(PB_ERR_INVALID_ARGUMENT, "fit needs at least two points");
+  std::vector<std::pair<int64_t, int64_t>> pts(n);
+  for (int32_t i = 0; i < n; ++i) pts[i] = {time[i], energy[i]};
+  std::stable_sort(pts.begin(), pts.end(),
+                   [](const auto& x, const auto& y) { return x.first < y.first; });
+  for (int32_t i = 0; i + 1 < n; ++i)
+    if (pts[i].first == pts[i + 1].first) return fail(PB_ERR_INVALID_ARGUMENT, "fit needs distinct times");
+  const double e_min = static_cast<double>(pts.back().second);
+  const double e_max = static_cast<double>(pts.front().second);
+  if (e_min == e_max) return fail(PB_ERR_DOMAIN, "all energies equal; treat the class as constant");
+  if (e_min > e_max) return fail(PB_ERR_INVALID_ARGUMENT, "fit expects energy decreasing with time");
+  if (n == 2) {
+    const double t1 = static_cast<double>(pts[0].first), t2 = static_cast<double>(pts[1].first);
+    const double e1 = static_cast<double>(pts[0].second), e2 = static_cast<double>(pts[1].second);
+    const double b = std::log(e2 / e1) / (t2 - t1);
+    out[0] = e1 * std::exp(-b * t1);
+    out[1] = b;
+    out[2] = 0.0;
+    out[3] = 0.0;
+    return PB_OK;
+  }
+  double lowest = e_min;
+  for (const auto& p : pts) lowest = std::min(lowest, static_cast<double>(p.second));
+  double best = -1.0;
+  for (int j = 0; j < 64; ++j) {
+    const double c = static_cast<double>(j) * (0.999 * lowest) / 63.0;
+    double st = 0, sy = 0, stt = 0, sty = 0;
+    for (const auto& p : pts) {
+      const double t = static_cast<double>(p.first);
+      const double y = std::log(static_cast<double>(p.second) - c);
+      st += t;
+      sy += y;
+      stt += t * t;
+      sty += t * y;
+    }
+    const double dn = static_cast<double>(n);
+    const double slope = (dn * sty - st * sy) / (dn * stt - st * st);
+    const double intercept = (sy - slope * st) / dn;
+    const double a = std::exp(intercept);
+    double sq = 0;
+    for (const auto& p : pts) {
+      const double r = a * std::exp(slope * static_cast<double>(p.first)) + c - static_cast<double>(p.second);
+      sq += r * r;
+    }
+    const double rmse = std::sqrt(sq / dn);
+    if (best < 0 || rmse < best) {
+      best = rmse;
+      out[0] = a;
+      out[1] = slope;
+      out[2] = c;
+      out[3] = rmse;
+    }
+  }
+  if (out[1] >= 0) return fail(PB_ERR_DOMAIN, "fitted exponent is not decreasing");
+  return PB_OK;
+}
+
+pb_status pb_batch_create(pb_batch** out) {
+  if (!out) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
+  *out = new pb_batch();
+  return PB_OK;
+}
+
+void pb_batch_destroy(pb_batch* b) { delete b; }
+
+int32_t pb_batch_size(const pb_batch* b) { return b ? static_cast<int32_t>(b->insts.size()) : 0; }
+
+pb_status pb_batch_add(pb_batch* b, const pb_instance_desc* d, int32_t* out_index) {
+  if (!b || !d) return fail(PB_ERR_INVALID_ARGUMENT, "null argument");
+  if (d->n < 0 || d->n_edges < 0 || d->n_classes < 0)
+    return fail(PB_ERR_INVALID_ARGUMENT, "negative size");
+  HostInst h;
+  h.n = d->n;
+  h.comp_class.assign(d->comp_class, d->comp_class + d->n);
+  h.edge_tail.assign(d->edge_tail, d->edge_tail + d->n_edges);
+  h.edge_head.assign(d->edge_head, d->edge_head + d->n_edges);
+  h.cls_const.assign(d->class_is_constant, d->class_is_constant + d->n_classes);
+  h.cls_pt_off.assign(d->class_point_off, d->class_point_off + d->n_classes + 1);
+  const int32_t np = h.cls_pt_off.empty() ? 0 : h.cls_pt_off.back();
+  if (!h.cls_pt_off.empty() && h.cls_pt_off.front() != 0)
+    return fail(PB_ERR_INVALID_ARGUMENT, "class point offsets must start at 0");
+  h.pt_freq.assign(d->point_freq, d->point_freq + np);
+  h.pt_time.assign(d->point_time, d->point_time + np);
+  h.pt_energy.assign(d->point_energy, d->point_energy + np);
+  h.cls_curve.assign(d->class_curve, d->class_curve + 3 * d->n_classes);
+  h.cls_trange.assign(d->class_t_range, d->class_t_range + 2 * d->n_classes);
+  h.watts = d->blocking_watts;
+  h.quantum = d->quantum_us;
+  h.tau = d->tau;
+  if (d->start_planned_t) h.start.assign(d->start_planned_t, d->start_planned_t + d->n);
+  h.max_steps = d->max_steps;
+  const pb_status s = validate_and_derive(h);
+  if (s != PB_OK) return s;
+  b->insts.push_back(std::move(h));
+  b->have_results = false;
+  if (out_index) *out_index = static_cast<int32_t>(b->insts.size()) - 1;
+  return PB_OK;
+}
+
+pb_status pb_batch_prepare(pb_batch* b, int32_t device) {
+  if (!b) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
+  return guarded([&] { return prepare_impl(b, device, 1.0); });
+}
+
+pb_status pb_batch_launch(pb_batch* b, double* kernel_ms) {
+  if (!b) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
+  return guarded([&] { return launch_impl(b, kernel_ms); });
+}
+
+pb_status pb_batch_fetch(pb_batch* b) {
+  if (!b) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
+  return guarded([&] { return fetch_impl(b); });
+}
+
+pb_status pb_batch_run(pb_batch* b, int32_t device) {
+  if (!b) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
+  return guarded([&] {
+    double scale = 1.0;
+    for (int attempt = 0; attempt < 6; ++attempt) {
+      pb_status s = prepare_impl(b, device, scale);
+      if (s != PB_OK) return s;
+      s = launch_impl(b, nullptr);
+      if (s != PB_OK) return s;
+      s = fetch_impl(b);
+      if (s != PB_OK) return s;
+      if (!any_log_full(b)) return PB_OK;
+      scale *= 4.0;  // rare: a walk took more steps than (T* - T_min) / tau
+    }
+    return fail(PB_ERR_LOGIC, "delta log kept overflowing");
+  });
+}
+
+pb_status pb_batch_run_multi(pb_batch* b, int32_t n_devices, const int32_t* devices) {
+  if (!b || n_devices < 1 || !devices) return fail(PB_ERR_INVALID_ARGUMENT, "bad device list");
+  if (n_devices == 1) return pb_batch_run(b, devices[0]);
+  return guarded([&]() -> pb_status {
+    // LPT over devices by estimated work; one sub-batch and host thread each.
+    const size_t N = b->insts.size();
+    std::vector<size_t> idx(N);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](size_t x, size_t y) { return b->insts[x].work > b->insts[y].work; });
+    std::vector<int64_t> load(n_devices, 0);
+    std::vector<std::vector<size_t>> part(n_devices);
+    for (size_t k : idx) {
+      const int d = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+      load[d] += b->insts[k].work;
+      part[d].push_back(k);
+    }
+    std::vector<pb_batch> subs(n_devices);
+    std::vector<pb_status> st(n_devices, PB_OK);
+    std::vector<std::thread> th;
+    for (int d = 0; d < n_devices; ++d) {
+      for (size_t k : part[d]) subs[d].insts.push_back(b->insts[k]);
+      th.emplace_back([&, d] { st[d] = pb_batch_run(&subs[d], devices[d]); });
+    }
+    for (auto& t : th) t.join();
+    for (int d = 0; d < n_devices; ++d)
+      if (st[d] != PB_OK) return st[d];
+    // stitch results back in the original order
+    b->run.release();
+    std::vector<char> out;
+    b->out_points.assign(N, 0);
+    b->out_ids.assign(N, 0);
+    b->out_choice.assign(N, 0);
+    b->out_summary.assign(N, 0);
+    b->cap_points.assign(N, 0);
+    b->cap_ids.assign(N, 0);
+    b->cls_tab.assign(N, {});
+    b->tables.clear();
+    b->stats = pb_run_stats{};
+    for (int d = 0; d < n_devices; ++d) {
+      const pb_batch& s = subs[d];
+      const size_t base = out.size();
+      out.insert(out.end(), s.out.begin(), s.out.end());
+      const int64_t tbase = static_cast<int64_t>(b->tables.size());
+      b->tables.insert(b->tables.end(), s.tables.begin(), s.tables.end());
+      for (size_t q = 0; q < part[d].size(); ++q) {
+        const size_t k = part[d][q];
+        b->out_points[k] = base + s.out_points[q];
+        b->out_ids[k] = base + s.out_ids[q];
+        b->out_choice[k] = base + s.out_choice[q];
+        b->out_summary[k] = base + s.out_summary[q];
+        b->cap_points[k] = s.cap_points[q];
+        b->cap_ids[k] = s.cap_ids[q];
+        b->cls_tab[k] = s.cls_tab[q];
+        for (auto& t : b->cls_tab[k]) t += tbase;
+      }
+      b->stats.kernel_ms = std::max(b->stats.kernel_ms, s.stats.kernel_ms);
+      b->stats.h2d_bytes += s.stats.h2d_bytes;
+      b->stats.d2h_bytes += s.stats.d2h_bytes;
+      b->stats.arc_scans += s.stats.arc_scans;
+      b->stats.node_updates += s.stats.node_updates;
+      b->stats.rounds += s.stats.rounds;
+      b->stats.kernel_launches += s.stats.kernel_launches;
+    }
+    b->out = std::move(out);
+    b->have_results = true;
+    return PB_OK;
+  });
+}
+
+pb_status pb_batch_summary(const pb_batch* b, int32_t k, pb_frontier_summary* out) {
+  if (!b || !out || k < 0 || k >= static_cast<int32_t>(b->insts.size()))
+    return fail(PB_ERR_INVALID_ARGUMENT, "bad instance index");
+  if (!b->have_results) return fail(PB_ERR_LOGIC, "batch has not been run");
+  *out = summary_of(b, k);
+  return PB_OK;
+}
+
+pb_status pb_batch_points(const pb_batch* b, int32_t k, pb_point* out, int32_t capacity) {
+  pb_frontier_summary s;
+  pb_status st = pb_batch_summary(b, k, &s);
+  if (st != PB_OK) return st;
+  const int32_t np = s.steps + 1;
+  if (capacity < np) return fail(PB_ERR_INVALID_ARGUMENT, "points buffer too small");
+  std::memcpy(out, b->out.data() + b->out_points[k], sizeof(pb_point) * np);
+  return PB_OK;
+}
+
+pb_status pb_batch_deltas(const pb_batch* b, int32_t k, int32_t* ids, uint8_t* choice,
+                          int32_t capacity) {
+  pb_frontier_summary s;
+  pb_status st = pb_batch_summary(b, k, &s);
+  if (st != PB_OK) return st;
+  if (capacity < s.n_ids) return fail(PB_ERR_INVALID_ARGUMENT, "delta buffer too small");
+  if (ids) std::memcpy(ids, b->out.data() + b->out_ids[k], sizeof(int32_t) * s.n_ids);
+  if (choice) std::memcpy(choice, b->out.data() + b->out_choice[k], s.n_ids);
+  return PB_OK;
+}
+
+pb_status pb_batch_schedule(const pb_batch* b, int32_t k, int32_t which, int64_t* planned_t,
+                            int64_t* planned_e, int32_t* freq_mhz, int64_t* realized_t,
+                            int64_t* realized_e, double* eff_planned, double* eff_realized) {
+  pb_frontier_summary s;
+  pb_status st = pb_batch_summary(b, k, &s);
+  if (st != PB_OK) return st;
+  if (which < 0 || which > s.steps) return fail(PB_ERR_INVALID_ARGUMENT, "schedule index out of range");
+  const HostInst& h = b->insts[k];
+  const int32_t n = h.n;
+  std::vector<int64_t> pt(n);
+  std::vector<int32_t> ch(n);
+  auto choose = [&](int32_t c, int64_t t) {
+    int32_t chosen = 0;
+    for (int32_t p = h.cls_pt_off[c]; p < h.cls_pt_off[c + 1]; ++p)
+      if (h.pt_time[p] <= t) chosen = p - h.cls_pt_off[c];
+    return chosen;
+  };
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t c = h.comp_class[i];
+    pt[i] = !h.start.empty() ? h.start[i] : (h.cls_const[c] ? h.pt_time[h.cls_pt_off[c]] : h.cls_trange[2 * c + 1]);
+    ch[i] = choose(c, pt[i]);
+  }
+  const pb_point* pts = reinterpret_cast<const pb_point*>(b->out.data() + b->out_points[k]);
+  const int32_t* ids = reinterpret_cast<const int32_t*>(b->out.data() + b->out_ids[k]);
+  const uint8_t* cho = reinterpret_cast<const uint8_t*>(b->out.data() + b->out_choice[k]);
+  for (int32_t q = 1; q <= which; ++q) {
+    const pb_point& p = pts[q];
+    const int32_t cnt = p.n_sped + p.n_slowed;
+    for (int32_t j = p.id_begin; j < p.id_begin + cnt; ++j) {
+      const int32_t x = ids[j];
+      const int32_t i = (x > 0 ? x : -x) - 1;
+      pt[i] += x > 0 ? -p.step_size : p.step_size;
+      ch[i] = cho[j];
+    }
+  }
+  double effp = 0, effr = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t c = h.comp_class[i];
+    const int32_t p = h.cls_pt_off[c] + ch[i];
+    int64_t e;
+    if (h.cls_const[c]) {
+      e = h.pt_energy[h.cls_pt_off[c]];
+    } else {
+      const int64_t lo = h.cls_trange[2 * c], hi = h.cls_trange[2 * c + 1];
+      const int64_t t = pt[i];
+      const double v = (t >= lo && t <= hi)
+                           ? b->tables[b->cls_tab[k][c] + (t - lo)]
+                           : h.cls_curve[3 * c] * std::exp(h.cls_curve[3 * c + 1] * static_cast<double>(t)) +
+                                 h.cls_curve[3 * c + 2];
+      e = static_cast<int64_t>(std::llround(v));
+    }
+    if (planned_t) planned_t[i] = pt[i];
+    if (planned_e) planned_e[i] = e;
+    if (freq_mhz) freq_mhz[i] = h.pt_freq[p];
+    if (realized_t) realized_t[i] = h.pt_time[p];
+    if (realized_e) realized_e[i] = h.pt_energy[p];
+    // effective_total (frontier.hpp:51-57; units.hpp:38-48), index order
+    effp += static_cast<double>(e) - h.watts * static_cast<double>(pt[i]) * static_cast<double>(h.quantum) * 1e-3;
+    effr += static_cast<double>(h.pt_energy[p]) -
+            h.watts * static_cast<double>(h.pt_time[p]) * static_cast<double>(h.quantum) * 1e-3;
+  }
+  if (eff_planned) *eff_planned = effp;
+  if (eff_realized) *eff_realized = effr;
+  return PB_OK;
+}
+
+pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out) {
+  if (!b || !out) return fail(PB_ERR_INVALID_ARGUMENT, "null argument");
+  *out = b->stats;
+  return PB_OK;
+}
+
+// ------------------------------------------------------- component kernels
+
+pb_status pb_annotate_slack_batch(int32_t device, int32_t count, const int32_t* n, const int32_t* ne,
+                                  const int32_t* edge_tail, const int32_t* edge_head,
+                                  const int64_t* durations, int64_t* earliest, int64_t* latest,
+                                  uint8_t* critical, int64_t* makespan) {
+  return guarded([&]() -> pb_status {
+    if (count <= 0) return PB_OK;
+    std::vector<HostInst> hs(count);
+    size_t eo = 0, dofs = 0;
+    for (int32_t g = 0; g < count; ++g) {
+      HostInst& h = hs[g];
+      h.n = n[g];
+      h.edge_tail.assign(edge_tail + eo, edge_tail + eo + ne[g]);
+      h.edge_head.assign(edge_head + eo, edge_head + eo + ne[g]);
+      eo += ne[g];
+      // one constant class so that validation passes; durations come separately
+      h.comp_class.assign(h.n, 0);
+      h.cls_const = {1};
+      h.cls_pt_off = {0, 1};
+      h.pt_freq = {1};
+      h.pt_time = {0};
+      h.pt_energy = {1};
+      h.cls_curve = {0, 0, 0};
+      h.cls_trange = {0, 0};
+      for (int32_t i = 0; i < h.n; ++i)
+        if (durations[dofs + i] < 0) return fail(PB_ERR_INVALID_ARGUMENT, "durations must be non-negative");
+      dofs += h.n;
+      const pb_status s = validate_and_derive(h);
+      if (s != PB_OK) return s;
+    }
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    Blob blob;
+    std::vector<std::array<size_t, 8>> off(count);
+    size_t out_e = 0, out_l = 0, out_c = 0;
+    std::vector<size_t> o_e(count), o_l(count), o_c(count), o_d(count);
+    int64_t max_n = 1, max_v = 1, max_e = 1;
+    dofs = 0;
+    for (int32_t g = 0; g < count; ++g) {
+      const HostInst& h = hs[g];
+      off[g] = {blob.put(h.lvl_off), blob.put(h.lvl_comps), blob.put(h.in_off), blob.put(h.in_dep),
+                blob.put(h.out_off), blob.put(h.out_dep), blob.put(h.snk_dep), 0};
+      off[g][7] = blob.put(h.edge_tail);
+      o_d[g] = blob.put(durations + dofs, sizeof(int64_t) * h.n);
+      dofs += h.n;
+      o_e[g] = out_e;
+      o_l[g] = out_l;
+      out_e += 2 * h.n + 2;
+      out_l += 2 * h.n + 2;
+      o_c[g] = out_c;
+      out_c += h.n + h.edge_tail.size();
+      max_n = std::max<int64_t>(max_n, h.n);
+      max_v = std::max<int64_t>(max_v, 2 * int64_t{h.n} + 2);
+      max_e = std::max<int64_t>(max_e, h.n + static_cast<int64_t>(h.edge_tail.size()) + 1);
+    }
+    std::vector<size_t> o_h(count);
+    for (int32_t g = 0; g < count; ++g) o_h[g] = blob.put(hs[g].edge_head);
+    char *d_blob = nullptr, *d_ws = nullptr;
+    int64_t *d_e = nullptr, *d_l = nullptr, *d_ms = nullptr;
+    uint8_t* d_c = nullptr;
+    pb::DevInst* d_insts = nullptr;
+    pb::SlackOut* d_outs = nullptr;
+    const pb::WsLayout ws = pb::make_ws_layout(max_n, max_v, max_e);
+    const int32_t slots = std::min<int32_t>(count, 1024);
+    ck(cudaMalloc(&d_blob, std::max<size_t>(blob.bytes.size(), 256)), "malloc");
+    ck(cudaMalloc(&d_e, sizeof(int64_t) * out_e), "malloc");
+    ck(cudaMalloc(&d_l, sizeof(int64_t) * out_l), "malloc");
+    ck(cudaMalloc(&d_c, std::max<size_t>(out_c, 1)), "malloc");
+    ck(cudaMalloc(&d_ms, sizeof(int64_t) * count), "malloc");
+    ck(cudaMalloc(&d_ws, static_cast<size_t>(ws.stride) * slots), "malloc");
+    ck(cudaMalloc(&d_insts, sizeof(pb::DevInst) * count), "malloc");
+    ck(cudaMalloc(&d_outs, sizeof(pb::SlackOut) * count), "malloc");
+    ck(cudaMemcpy(d_blob, blob.bytes.data(), blob.bytes.size(), cudaMemcpyHostToDevice), "H2D");
+    std::vector<pb::DevInst> di(count);
+    std::vector<pb::SlackOut> so(count);
+    for (int32_t g = 0; g < count; ++g) {
+      const HostInst& h = hs[g];
+      pb::DevInst& d = di[g];
+      d.n = h.n;
+      d.ne = static_cast<int32_t>(h.edge_tail.size());
+      d.n_levels = h.n_levels;
+      d.lvl_off = dptr<int32_t>(d_blob, off[g][0]);
+      d.lvl_comps = dptr<int32_t>(d_blob, off[g][1]);
+      d.in_off = dptr<int32_t>(d_blob, off[g][2]);
+      d.in_dep = dptr<int32_t>(d_blob, off[g][3]);
+      d.out_off = dptr<int32_t>(d_blob, off[g][4]);
+      d.out_dep = dptr<int32_t>(d_blob, off[g][5]);
+      d.snk_dep = dptr<int32_t>(d_blob, off[g][6]);
+      d.n_snk = static_cast<int32_t>(h.snk_dep.size());
+      d.dep_tail = dptr<int32_t>(d_blob, off[g][7]);
+      d.dep_head = dptr<int32_t>(d_blob, o_h[g]);
+      so[g].dur = dptr<int64_t>(d_blob, o_d[g]);
+      so[g].earliest = d_e + o_e[g];
+      so[g].latest = d_l + o_l[g];
+      so[g].critical = d_c + o_c[g];
+    }
+    ck(cudaMemcpy(d_insts, di.data(), sizeof(pb::DevInst) * count, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(d_outs, so.data(), sizeof(pb::SlackOut) * count, cudaMemcpyHostToDevice), "H2D");
+    const int rc = pb::launch_slack_jobs(d_insts, d_outs, d_ms, count, d_ws, ws, slots, nullptr);
+    if (rc) throw CudaError(cudaGetErrorString(static_cast<cudaError_t>(rc)));
+    ck(cudaDeviceSynchronize(), "slack kernel");
+    ck(cudaMemcpy(earliest, d_e, sizeof(int64_t) * out_e, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(latest, d_l, sizeof(int64_t) * out_l, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(critical, d_c, out_c, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(makespan, d_ms, sizeof(int64_t) * count, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d_blob);
+    cudaFree(d_e);
+    cudaFree(d_l);
+    cudaFree(d_c);
+    cudaFree(d_ms);
+    cudaFree(d_ws);
+    cudaFree(d_insts);
+    cudaFree(d_outs);
+    return PB_OK;
+  });
+}
+
+pb_status pb_flow_min_cut_batch(int32_t device, int32_t count, const int32_t* nodes,
+                                const int32_t* source, const int32_t* sink, const int32_t* m,
+                                const int32_t* tail, const int32_t* head, const int64_t* lower,
+                                const int64_t* upper, const uint8_t* infinite, int32_t* status,
+                                uint8_t* feasible, int64_t* value, int64_t* sentinel,
+                                int64_t* cost, uint8_t* source_side, int8_t* cut_dir) {
+  return guarded([&]() -> pb_status {
+    if (count <= 0) return PB_OK;
+    // validation mirrors FlowGraph (flow.hpp:34-50, 71-77)
+    size_t eo = 0, no = 0;
+    for (int32_t g = 0; g < count; ++g) {
+      if (nodes[g] < 2) return fail(PB_ERR_INVALID_ARGUMENT, "flow graph needs at least two nodes");
+      if (source[g] == sink[g] || source[g] < 0 || sink[g] < 0 || source[g] >= nodes[g] || sink[g] >= nodes[g])
+        return fail(PB_ERR_INVALID_ARGUMENT, "invalid source/sink");
+      for (int32_t e = 0; e < m[g]; ++e) {
+        const size_t k = eo + e;
+        if (tail[k] < 0 || head[k] < 0 || tail[k] >= nodes[g] || head[k] >= nodes[g])
+          return fail(PB_ERR_INVALID_ARGUMENT, "edge endpoint out of range");
+        if (tail[k] == head[k]) return fail(PB_ERR_INVALID_ARGUMENT, "self-loops not allowed");
+        if (lower[k] < 0) return fail(PB_ERR_INVALID_ARGUMENT, "negative lower bound");
+        if (!infinite[k] && upper[k] < lower[k]) return fail(PB_ERR_INVALID_ARGUMENT, "upper bound below lower bound");
+      }
+      eo += m[g];
+      no += nodes[g];
+    }
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    Blob blob;
+    std::vector<std::array<size_t, 7>> off(count);
+    int64_t max_v = 2, max_e = 1;
+    eo = 0;
+    for (int32_t g = 0; g < count; ++g) {
+      const int32_t V = nodes[g], M = m[g];
+      std::vector<int32_t> t(tail + eo, tail + eo + M), h(head + eo, head + eo + M);
+      t.push_back(sink[g]);
+      h.push_back(source[g]);
+      std::vector<int32_t> io(V + 1, 0), inc(2 * (M + 1));
+      for (int32_t k = 0; k <= M; ++k) {
+        ++io[t[k] + 1];
+        ++io[h[k] + 1];
+      }
+      for (int32_t v = 0; v < V; ++v) io[v + 1] += io[v];
+      std::vector<int32_t> fill(io.begin(), io.end() - 1);
+      for (int32_t k = 0; k <= M; ++k) {
+        inc[fill[t[k]]++] = k << 1;
+        inc[fill[h[k]]++] = (k << 1) | 1;
+      }
+      off[g][0] = blob.put(io);
+      off[g][1] = blob.put(inc);
+      off[g][2] = blob.put(t);
+      off[g][3] = blob.put(h);
+      off[g][4] = blob.put(lower + eo, sizeof(int64_t) * M);
+      off[g][5] = blob.put(upper + eo, sizeof(int64_t) * M);
+      off[g][6] = blob.put(infinite + eo, M);
+      max_v = std::max<int64_t>(max_v, V);
+      max_e = std::max<int64_t>(max_e, M + 1);
+      eo += M;
+    }
+    const size_t E = eo, NV = no;
+    char *d_blob = nullptr, *d_ws = nullptr, *d_out = nullptr;
+    pb::DevFlowJob* d_jobs = nullptr;
+    // outputs: status, feasible, value, sentinel, cost, side, cut_dir
+    Blob outl;
+    const size_t o_st = outl.put(nullptr, 4 * count), o_fe = outl.put(nullptr, count),
+                 o_va = outl.put(nullptr, 8 * count), o_se = outl.put(nullptr, 8 * count),
+                 o_co = outl.put(nullptr, 8 * count), o_si = outl.put(nullptr, std::max<size_t>(NV, 1)),
+                 o_cd = outl.put(nullptr, std::max<size_t>(E, 1));
+    const pb::WsLayout ws = pb::make_ws_layout(1, max_v, max_e);
+    const int32_t slots = std::min<int32_t>(count, 1024);
+    ck(cudaMalloc(&d_blob, std::max<size_t>(blob.bytes.size(), 256)), "malloc");
+    ck(cudaMalloc(&d_out, outl.bytes.size()), "malloc");
+    ck(cudaMemset(d_out, 0, outl.bytes.size()), "memset");
+    ck(cudaMalloc(&d_ws, static_cast<size_t>(ws.stride) * slots), "malloc");
+    ck(cudaMalloc(&d_jobs, sizeof(pb::DevFlowJob) * count), "malloc");
+    ck(cudaMemcpy(d_blob, blob.bytes.data(), blob.bytes.size(), cudaMemcpyHostToDevice), "H2D");
+    std::vector<pb::DevFlowJob> jobs(count);
+    eo = 0;
+    no = 0;
+    for (int32_t g = 0; g < count; ++g) {
+      pb::DevFlowJob& j = jobs[g];
+      j.nodes = nodes[g];
+      j.source = source[g];
+      j.sink = sink[g];
+      j.m = m[g];
+      j.inc_off = dptr<int32_t>(d_blob, off[g][0]);
+      j.inc = dptr<int32_t>(d_blob, off[g][1]);
+      j.tail = dptr<int32_t>(d_blob, off[g][2]);
+      j.head = dptr<int32_t>(d_blob, off[g][3]);
+      j.lower = dptr<int64_t>(d_blob, off[g][4]);
+      j.upper = dptr<int64_t>(d_blob, off[g][5]);
+      j.inf = dptr<uint8_t>(d_blob, off[g][6]);
+      j.status = reinterpret_cast<int32_t*>(d_out + o_st);
+      j.feasible = reinterpret_cast<uint8_t*>(d_out + o_fe);
+      j.value = reinterpret_cast<int64_t*>(d_out + o_va);
+      j.sentinel = reinterpret_cast<int64_t*>(d_out + o_se);
+      j.cost = reinterpret_cast<int64_t*>(d_out + o_co);
+      j.side = reinterpret_cast<uint8_t*>(d_out + o_si) + no;
+      j.cut_dir = reinterpret_cast<int8_t*>(d_out + o_cd) + eo;
+      eo += m[g];
+      no += nodes[g];
+    }
+    ck(cudaMemcpy(d_jobs, jobs.data(), sizeof(pb::DevFlowJob) * count, cudaMemcpyHostToDevice), "H2D");
+    const int rc = pb::launch_flow_jobs(d_jobs, count, d_ws, ws, slots, nullptr);
+    if (rc) throw CudaError(cudaGetErrorString(static_cast<cudaError_t>(rc)));
+    ck(cudaDeviceSynchronize(), "flow kernel");
+    std::vector<char> host(outl.bytes.size());
+    ck(cudaMemcpy(host.data(), d_out, host.size(), cudaMemcpyDeviceToHost), "D2H");
+    std::memcpy(status, host.data() + o_st, 4 * count);
+    std::memcpy(feasible, host.data() + o_fe, count);
+    std::memcpy(value, host.data() + o_va, 8 * count);
+    std::memcpy(sentinel, host.data() + o_se, 8 * count);
+    std::memcpy(cost, host.data() + o_co, 8 * count);
+    std::memcpy(source_side, host.data() + o_si, NV);
+    std::memcpy(cut_dir, host.data() + o_cd, E);
+    cudaFree(d_blob);
+    cudaFree(d_out);
+    cudaFree(d_ws);
+    cudaFree(d_jobs);
+    return PB_OK;
+  });
+}
+
+// ------------------------------------------------------------------- G9
+
+pb_status pb_g9_stage_bases(int32_t stages, int32_t base, double imbalance, uint32_t seed,
+                            int32_t straggler_stage, double phi, int32_t* out_bases) {
+  if (stages < 1) return fail(PB_ERR_INVALID_ARGUMENT, "pipeline needs at least one stage");
+  pb_g9::Params p;
+  p.stages = stages;
+  p.base = base;
+  p.imbalance = imbalance;
+  p.seed = seed;
+  p.straggler_stage = straggler_stage;
+  p.phi = phi;
+  const auto b = pb_g9::stage_bases(p);
+  std::copy(b.begin(), b.end(), out_bases);
+  return PB_OK;
+}
+
+pb_status pb_g9_batch_params(int32_t i, int32_t* stages, int32_t* microbatches, double* imbalance,
+                             double* phi, int32_t* straggler, uint32_t* seed) {
+  const pb_g9::Params p = pb_g9::batch_instance(i);
+  *stages = p.stages;
+  *microbatches = p.microbatches;
+  *imbalance = p.imbalance;
+  *phi = p.phi;
+  *straggler = p.straggler_stage;
+  *seed = p.seed;
+  return PB_OK;
+}
+
+pb_status pb_g9_profile(int32_t b, int32_t backward, int64_t tau, int32_t* freq, int64_t* time,
+                        int64_t* energy) {
+  const auto pts = pb_g9::stage_profile(b, backward != 0, tau);
+  for (size_t j = 0; j < pts.size(); ++j) {
+    freq[j] = pts[j].freq_mhz;
+    time[j] = pts[j].time;
+    energy[j] = pts[j].energy;
+  }
+  return PB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// Internal layout shared by the host packer (pb_host.cpp) and the sm_100a
+// kernels (pb_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+
+#include "perseus_b200.h"
+
+namespace pb {
+
+// Walk modes.
+enum : int32_t { kModeDiscover = 0, kModeGetNext = 1 };
+
+// Internal per-instance status beyond pb_status.
+enum : int32_t { kStatusLogFull = 100 };
+
+// One packed instance: every pointer is a DEVICE address into the batch blob
+// (static data) or the output blob.  Node-DAG ids: computations 0..n-1,
+// virtual source n, sink n+1.  Edge-centric ids (dag.hpp:209-224):
+// computation i -> edge i from node 2i to 2i+1; dependency j -> edge n+j;
+// edge n+ne is the phase-A return arc sink->source (flow.hpp:196-200).
+struct DevInst {
+  int32_t n, ne, n_levels, mode;
+  int32_t max_steps, cap_points, cap_ids, pad0;
+  int64_t tau;
+  double watts;
+  int64_t quantum;
+  // node DAG
+  const int32_t* comp_class;  // [n]
+  const int32_t* lvl_off;     // [n_levels + 1]
+  const int32_t* lvl_comps;   // [n], topological levels (Kahn depth)
+  const int32_t* in_off;      // [n + 1]
+  const int32_t* in_dep;      // dependency ids j with head == comp
+  const int32_t* out_off;     // [n + 1]
+  const int32_t* out_dep;     // dependency ids j with tail == comp
+  const int32_t* snk_dep;     // dependency ids j with head == sink
+  int32_t n_snk, pad1;
+  const int32_t* dep_tail;  // [ne] node-DAG ids
+  const int32_t* dep_head;  // [ne]
+  // edge-centric incidence (flow network), V = 2n + 2 nodes, E = n + ne + 1
+  const int32_t* inc_off;  // [V + 1]
+  const int32_t* inc;      // (edge << 1) | dir, dir = 1 when the node is the head
+  const int32_t* ec_tail;  // [E]
+  const int32_t* ec_head;  // [E]
+  // cost model
+  const uint8_t* cls_const;   // [classes]
+  const int64_t* cls_tmin;    // [classes] curve t_min (table origin)
+  const int64_t* cls_tmax;    // [classes]
+  const int64_t* cls_tab;     // [classes] offset of E(t_min) in tables
+  const int32_t* cls_pt_off;  // [classes + 1]
+  const int64_t* pt_time;
+  const int64_t* pt_energy;
+  const double* tables;           // E(t) = a exp(b t) + c for t in [t_min, t_max]
+  const int64_t* start_planned_t; // get-next mode only
+  // outputs
+  pb_point* points;             // [cap_points]
+  int32_t* ids;                 // [cap_ids]
+  uint8_t* choice;              // [cap_ids]
+  pb_frontier_summary* summary; // [1]
+};
+
+// Per-CTA workspace slot; arrays sized for the largest instance of a batch.
+struct WsLayout {
+  int64_t max_n, max_v, max_e;
+  int64_t off_excess, off_tres, off_height, off_mark, off_nr, off_side;
+  int64_t off_lower, off_cap, off_flow, off_einf, off_ecrit;
+  int64_t off_planned, off_estart, off_lend, off_rstart, off_rdur, off_pdur, off_choice;
+  int64_t off_list0, off_list1, off_bfs0, off_bfs1, off_dead, off_dem, off_delta;
+  int64_t stride;
+};
+
+struct RunCounters {
+  unsigned long long arc_scans;
+  unsigned long long node_updates;
+  unsigned long long rounds;
+  unsigned long long comp_visits;
+};
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
+  WsLayout L{};
+  L.max_n = max_n;
+  L.max_v = max_v;
+  L.max_e = max_e;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  L.off_excess = take(8 * max_v);
+  L.off_tres = take(8 * max_v);
+  L.off_height = take(4 * max_v);
+  L.off_mark = take(4 * max_v);
+  L.off_nr = take(max_v);
+  L.off_side = take(4 * max_v);
+  L.off_lower = take(8 * max_e);
+  L.off_cap = take(8 * max_e);
+  L.off_flow = take(8 * max_e);
+  L.off_einf = take(max_e);
+  L.off_ecrit = take(max_e);
+  L.off_planned = take(8 * max_n);
+  L.off_estart = take(8 * max_n);
+  L.off_lend = take(8 * max_n);
+  L.off_rstart = take(8 * max_n);
+  L.off_rdur = take(8 * max_n);
+  L.off_pdur = take(8 * max_n);
+  L.off_choice = take(max_n);
+  L.off_list0 = take(4 * max_v);
+  L.off_list1 = take(4 * max_v);
+  L.off_bfs0 = take(4 * max_v);
+  L.off_bfs1 = take(4 * max_v);
+  L.off_dead = take(4 * max_v);
+  L.off_dem = take(4 * max_n);
+  L.off_delta = take(4 * max_n);
+  L.stride = o;
+  return L;
+}
+
+// Generic flow-graph job for pb_flow_min_cut_batch: the same push-relabel
+// device code on an arbitrary FlowGraph (flow.hpp:22-80).
+struct DevFlowJob {
+  int32_t nodes, source, sink, m;
+  const int32_t* inc_off;  // [nodes + 1]
+  const int32_t* inc;      // (edge << 1) | dir
+  const int32_t* tail;     // [m + 1], edge m = return arc sink -> source
+  const int32_t* head;
+  const int64_t* lower;    // [m]
+  const int64_t* upper;    // [m]
+  const uint8_t* inf;      // [m]
+  // outputs
+  int32_t* status;
+  uint8_t* feasible;
+  int64_t* value;
+  int64_t* sentinel;
+  int64_t* cost;
+  uint8_t* side;   // [nodes]
+  int8_t* cut_dir; // [m]
+};
+
+// Host-side launchers (pb_kernels.cu).
+int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
+                 char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
+                 void* stream);
+int walk_slots_per_sm();
+int launch_flow_jobs(const DevFlowJob* d_jobs, int32_t count, char* d_ws, const WsLayout& ws,
+                     int32_t slots, void* stream);
+// annotate_slack job outputs (per DAG).
+struct SlackOut {
+  const int64_t* dur;
+  int64_t* earliest;
+  int64_t* latest;
+  uint8_t* critical;
+};
+int launch_slack_jobs(const DevInst* d_insts, const SlackOut* d_outs, int64_t* d_makespan,
+                      int32_t count, char* d_ws, const WsLayout& ws, int32_t slots, void* stream);
+
+}  // namespace pb

@@ -1,0 +1,58 @@
+"""Regenerates the golden fixtures in tests/golden/ by running the UNMODIFIED
+reference (oracle/_ref/ref_driver, built from /root/reference by
+`make -C oracle ref`).  Run in the build container:
+
+    python tests/golden/make_golden.py
+
+Fixtures (JSON lines, gzip):
+  walks.jsonl.gz      frontier walks: the reference's own golden instances
+                      (diamond, lone, clip, ten-tau), G9 configs 1-2, random
+                      grid-profile walks (testutil::grid_profiles) and random
+                      cubic-profile walks (infeasible / infinite-cut stops)
+  flow424242.jsonl.gz acceptance gate 3 corpus: 1000 random bounded graphs,
+                      seed 424242, <= 12 nodes (acceptance.cpp:137-157)
+  flow7302.jsonl.gz   test_flow.cpp:90-114 corpus: 600 graphs, seed 7302
+  slack7102.jsonl.gz  annotate_slack on random DAGs (test_dag.cpp:244-263 style)
+  batch_small.jsonl.gz  small config-5 style G9 instances (summaries only)
+"""
+import gzip
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+
+
+def run(*args):
+    out = subprocess.run([DRIVER, *args], check=True, capture_output=True, text=True)
+    return [line for line in out.stdout.splitlines() if line.strip()]
+
+
+def write(name, lines):
+    path = os.path.join(HERE, name)
+    with gzip.open(path, "wt") as f:
+        for line in lines:
+            f.write(line + "\n")
+    print(f"{name}: {len(lines)} records, {os.path.getsize(path)} bytes")
+
+
+def main():
+    if not os.path.exists(DRIVER):
+        sys.exit("build the reference driver first: make -C oracle ref")
+    walk_specs = ["diamond", "lone:1000:9000:3000:5000", "lone:1000:9000:3000:5000:800",
+                  "lone:1000:5000:11000:800", "config:1", "config:2"]
+    walk_specs += [f"grid:{s}:{1 + s % 3}:{1 + s % 4}" for s in range(1, 41)]
+    walk_specs += [f"grid:{s}:{2 + s % 3}:{2 + s % 5}:4" for s in range(100, 120)]
+    walk_specs += [f"cubic:{s}:{1 + s % 4}:{1 + s % 6}" for s in range(1, 41)]
+    walk_specs += [f"g9:{2 + s % 5}:{2 + s % 7}:{8 + s % 4}:1.2:{s}:{s % 3 - 1}:1.5" for s in range(1, 21)]
+    write("walks.jsonl.gz", run("walkcheck", *walk_specs))
+    write("flow424242.jsonl.gz", run("flow", "424242", "1000", "12", "30"))
+    write("flow7302.jsonl.gz", run("flow", "7302", "600", "8", "30"))
+    write("slack7102.jsonl.gz", run("slack", "7102", "200"))
+
+
+if __name__ == "__main__":
+    main()

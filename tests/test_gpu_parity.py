@@ -1,0 +1,258 @@
+"""GPU parity: the sm_100a frontier walk (through the C ABI) against the
+reference's outputs (golden fixtures from the unmodified reference) and the
+CPU oracle.  Bit-exact for every integer field; energies within 1e-9
+relative (north_star) -- and bit-exact when materialized through
+pb_batch_schedule, which sums in reference order."""
+import numpy as np
+import pytest
+
+import paper_2312_06902_b200 as pb
+from paper_2312_06902_b200 import g9
+from paper_2312_06902_b200.model import (ClassKey, Computation, CostModel, FrequencyProfile, Kind,
+                                         PackedInstance, ProfilePoint, ProfileSet, finalize_custom_dag)
+from oracle import port
+
+from fixtures import instance_from_golden
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-9  # north_star energy tolerance
+
+
+def _eff(sum_e, sum_t, watts, q):
+    return float(sum_e) - watts * float(sum_t) * float(q) * 1e-3
+
+
+def check_walk_against(batch, k, w, watts, q, full=True):
+    s = batch.summary(k)
+    assert s.status == 0
+    assert pb.STOP_NAMES[s.stop] == w["reason"], (w["spec"], pb.STOP_NAMES[s.stop], w["reason"])
+    assert (s.t_min, s.t_star, s.steps) == (w["t_min"], w["t_star"], w["steps"]), w["spec"]
+    pts = batch.points(k)
+    assert pts["t_planned"].tolist() == w["t_planned"], w["spec"]
+    assert pts["t_realized"].tolist() == w["t_realized"], w["spec"]
+    assert pts["sum_planned_e"].tolist() == w["sum_planned_e"], w["spec"]
+    assert pts["sum_realized_e"].tolist() == w["sum_realized_e"], w["spec"]
+    assert pts["cut_cost"][1:].tolist() == w["cut_cost"], w["spec"]
+    assert pts["step_size"][1:].tolist() == w["step_size"], w["spec"]
+    ids, _ = batch.deltas(k)
+    for j in range(1, s.steps + 1):
+        p = pts[j]
+        seg = ids[p["id_begin"]:p["id_begin"] + p["n_sped"] + p["n_slowed"]]
+        assert [int(x) - 1 for x in seg if x > 0] == w["sped"][j - 1], (w["spec"], j)
+        assert [int(-x) - 1 for x in seg if x < 0] == w["slowed"][j - 1], (w["spec"], j)
+    for j in range(s.steps + 1):
+        ep = _eff(pts["sum_planned_e"][j], pts["sum_planned_t"][j], watts, q)
+        er = _eff(pts["sum_realized_e"][j], pts["sum_realized_t"][j], watts, q)
+        assert abs(ep - w["eff_planned"][j]) <= REL * max(1.0, abs(w["eff_planned"][j]))
+        assert abs(er - w["eff_realized"][j]) <= REL * max(1.0, abs(w["eff_realized"][j]))
+    if full:
+        for j in range(s.steps + 1):
+            d = batch.schedule(k, j)
+            h = port.schedule_hash(d.planned_t, d.planned_e, d.freq_mhz, d.realized_t, d.realized_e)
+            assert h == w["hash"][j], (w["spec"], j)
+            assert d.eff_planned_mj == w["eff_planned"][j]
+            assert d.eff_realized_mj == w["eff_realized"][j]
+
+
+def test_every_golden_walk_in_one_batch(walks):
+    """All 126 reference walks (golden instances, G9 configs 1-2, random grid
+    and cubic profiles with infeasible / infinite-cut stops) as ONE batch."""
+    b = pb.FrontierBatch()
+    meta = []
+    for spec, w in walks.items():
+        dag, model, tau = instance_from_golden(w)
+        b.add(dag, model, tau)
+        meta.append((spec, model))
+    b.run(0)
+    for k, (spec, model) in enumerate(meta):
+        check_walk_against(b, k, walks[spec], model.blocking_watts, model.quantum_us, full=spec != "config:2")
+
+
+def test_config2_every_point_bit_exact(walks):
+    w = walks["config:2"]
+    dag, model, tau = instance_from_golden(w)
+    b = pb.FrontierBatch()
+    b.add(dag, model, tau)
+    b.run(0)
+    check_walk_against(b, 0, w, model.blocking_watts, model.quantum_us, full=True)
+
+
+def test_walks_individually_match_batched(walks):
+    specs = [s for s in walks if s.startswith("cubic")][:6]
+    for spec in specs:
+        w = walks[spec]
+        dag, model, tau = instance_from_golden(w)
+        b = pb.FrontierBatch()
+        b.add(dag, model, tau)
+        b.run(0)
+        check_walk_against(b, 0, w, model.blocking_watts, model.quantum_us)
+
+
+def test_random_g9_instances_vs_oracle():
+    """Small G9 instances drawn like config 5, checked against the C oracle."""
+    b = pb.FrontierBatch()
+    packs = []
+    rng = np.random.default_rng(11)
+    for i in range(24):
+        p = g9.G9Params(int(rng.integers(2, 6)), int(rng.integers(2, 12)), int(rng.integers(8, 12)),
+                        float(rng.uniform(1.0, 1.25)), int(rng.integers(0, 2**31)),
+                        int(rng.integers(-1, 3)), float(rng.choice([1.0, 1.05, 1.1, 1.2, 1.3, 1.5])))
+        if p.straggler_stage >= p.stages:
+            p.straggler_stage = -1
+        dag, model = g9.instance(p)
+        b.add(dag, model, g9.TAU)
+        packs.append(PackedInstance(dag, model, g9.TAU))
+    b.run(0)
+    for k, P in enumerate(packs):
+        ref = port.discover_frontier(P, g9.TAU)
+        s = b.summary(k)
+        pts = b.points(k)
+        assert s.steps == ref["steps"] and pb.STOP_NAMES[s.stop] == ref["reason"]
+        assert pts["t_planned"].tolist() == ref["t_planned"]
+        assert pts["t_realized"].tolist() == ref["t_realized"]
+        assert pts["cut_cost"][1:].tolist() == ref["cut_cost"]
+        last = b.schedule(k, s.steps)
+        assert last.planned_t == ref["final_planned_t"] and last.freq_mhz == ref["final_freq"]
+
+
+# ---- the reference API, test_frontier.cpp style -----------------------------
+
+def _lone(ft, fe, st, se):
+    dag = finalize_custom_dag([Computation(0, 0, 0, Kind.Forward)], [])
+    m = CostModel.build(ProfileSet(75.0, [FrequencyProfile(ClassKey(0, 0), [ProfilePoint(1400, ft, fe),
+                                                                            ProfilePoint(1000, st, se)])]))
+    return dag, m
+
+
+def _diamond():
+    comps = [Computation(i, i, 0, Kind.Forward) for i in range(5)]
+    dag = finalize_custom_dag(comps, [(0, 1), (1, 2), (0, 3), (4, 2)])
+
+    def two(stage, t0, e0, t1, e1):
+        return FrequencyProfile(ClassKey(stage, 0), [ProfilePoint(1400, t0, e0), ProfilePoint(1000, t1, e1)])
+    m = CostModel.build(ProfileSet(75.0, [two(0, 1000, 4000, 3000, 1000), two(1, 1000, 625, 3000, 400),
+                                          two(2, 1000, 4000, 3000, 1000), two(3, 4000, 625, 6000, 400),
+                                          two(4, 4000, 625, 6000, 400)]))
+    return dag, m
+
+
+def test_min_energy_seed():
+    dag, m = _lone(1000, 9000, 2000, 5000)
+    s = pb.min_energy_schedule(dag, m)  # test_frontier.cpp:70-78
+    assert s.planned_t == [2000] and s.planned_e == [5000] and s.t_planned == 2000
+    assert s.eff_planned_mj == pytest.approx(5000 - 0.075 * 2000)
+    assert not s.discretized()
+
+
+def test_all_max_schedule():
+    dag, m = _diamond()
+    s = pb.all_max_schedule(dag, m)  # test_frontier.cpp:80-90
+    assert s.schedule_id == -1 and s.freq_mhz == [1400] * 5
+    assert s.planned_t == [1000, 1000, 1000, 4000, 4000] and s.realized_t == s.planned_t
+    assert s.t_planned == 5000 and s.t_realized == 5000
+    assert s.eff_planned_mj == pytest.approx(9875 - 0.075 * 11000)
+
+
+def test_lone_get_next_schedule():
+    dag, m = _lone(1000, 9000, 3000, 5000)
+    seed = pb.min_energy_schedule(dag, m)
+    info = pb.StepInfo()
+    mid = pb.get_next_schedule(dag, seed, m, 1000, info)  # test_frontier.cpp:120-144
+    assert mid.t_planned == 2000 and mid.planned_t == [2000] and mid.planned_e == [6708]
+    assert info.cut_cost == 1708 and info.sped_up == [0] and info.slowed_down == []
+    fast = pb.get_next_schedule(dag, mid, m, 1000, info)
+    assert fast.t_planned == 1000 and fast.planned_e == [9000] and info.cut_cost == 2292
+    assert pb.get_next_schedule(dag, fast, m, 1000) is None
+    with pytest.raises(ValueError):
+        pb.get_next_schedule(dag, seed, m, 0)
+    with pytest.raises(ValueError):
+        pb.discover_frontier(dag, m, 0)
+
+
+def test_diamond_step_by_step():
+    dag, m = _diamond()
+    cur = pb.min_energy_schedule(dag, m)
+    assert cur.t_planned == 9000 and cur.planned_t == [3000, 3000, 3000, 6000, 6000]
+    walk = [(300, [1, 3, 4], [], [3000, 2000, 3000, 5000, 5000]),
+            (375, [1, 3, 4], [], [3000, 1000, 3000, 4000, 4000]),
+            (1875, [0, 2], [1], [2000, 2000, 2000, 4000, 4000]),
+            (3900, [0, 2], [1], [1000, 3000, 1000, 4000, 4000])]
+    for cut, sped, slowed, planned in walk:  # test_frontier.cpp:177-212
+        info = pb.StepInfo()
+        nxt = pb.get_next_schedule(dag, cur, m, 1000, info)
+        assert (info.cut_cost, info.sped_up, info.slowed_down, nxt.planned_t) == (cut, sped, slowed, planned)
+        assert nxt.t_planned == cur.t_planned - 1000
+        assert sum(nxt.planned_e) - sum(cur.planned_e) == cut
+        cur = nxt
+    assert pb.get_next_schedule(dag, cur, m, 1000) is None
+
+
+def test_diamond_frontier_and_lookup():
+    dag, m = _diamond()
+    f = pb.discover_frontier(dag, m, 1000)  # test_frontier.cpp:214-265
+    assert len(f.schedules) == 5 and f.steps == 4 and f.t_star == 9000 and f.t_min == 5000
+    assert [s.t_planned for s in f.schedules] == [9000, 8000, 7000, 6000, 5000]
+    assert [s.t_realized for s in f.schedules] == [9000, 7000, 7000, 5000, 5000]
+    assert [sum(s.planned_e) for s in f.schedules] == [3200, 3500, 3875, 5750, 9650]
+    assert [s.eff_planned_mj for s in f.schedules] == pytest.approx([1625, 2150, 2750, 4700, 8675])
+    assert f.schedules[1].freq_mhz == f.schedules[2].freq_mhz
+    for s in f.schedules:
+        assert all(r <= p for r, p in zip(s.realized_t, s.planned_t))
+    am = pb.all_max_schedule(dag, m)
+    assert f.schedules[-1].t_realized == am.t_realized
+    assert f.schedules[-1].eff_realized_mj < am.eff_realized_mj
+    ids = [pb.lookup(f, t).schedule_id for t in (9000, 250000, 8999, 7500, 7000, 5000, 4999, 0)]
+    assert ids == [0, 0, 1, 2, 2, 4, 4, 4]
+    with pytest.raises(pb.LogicError):
+        pb.lookup(pb.Frontier(), 1000)
+
+
+def test_all_constant_classes_single_point():
+    dag = finalize_custom_dag([Computation(0, 0, 0, Kind.Forward), Computation(1, 1, 0, Kind.Forward)], [(0, 1)])
+    m = CostModel.build(ProfileSet(75.0, [
+        FrequencyProfile(ClassKey(0, 0), [ProfilePoint(1400, 2000, 3000), ProfilePoint(1200, 2500, 3100)]),
+        FrequencyProfile(ClassKey(1, 0), [ProfilePoint(1400, 1500, 2000), ProfilePoint(1200, 1600, 2400)])]))
+    seed = pb.min_energy_schedule(dag, m)  # test_frontier.cpp:92-116
+    assert seed.planned_t == pb.all_max_schedule(dag, m).planned_t
+    assert pb.get_next_schedule(dag, seed, m, 1000) is None
+    f = pb.discover_frontier(dag, m, 1000)
+    assert len(f.schedules) == 1 and f.steps == 0 and f.t_star == f.t_min == 3500
+    assert pb.lookup(f, 0) is f.schedules[0] and pb.lookup(f, 100000) is f.schedules[0]
+
+
+def test_discretize_cases():
+    dag = finalize_custom_dag([Computation(0, 0, 0, Kind.Forward)], [])
+    m = CostModel.build(ProfileSet(75.0, [FrequencyProfile(ClassKey(0, 0), [
+        ProfilePoint(1410, 1900, 900), ProfilePoint(1200, 2300, 700), ProfilePoint(1000, 2800, 500)])]))
+    for planned, freq, rt in [(2400, 1200, 2300), (2300, 1200, 2300), (1500, 1410, 1900), (5000, 1000, 2800)]:
+        s = pb.EnergySchedule(planned_t=[planned], planned_e=[700], t_planned=planned)
+        d = pb.discretize(s, dag, m)  # test_frontier.cpp:269-309
+        assert d.freq_mhz == [freq] and d.realized_t == [rt] and d.t_realized == rt
+
+
+# ---- full-size properties (BASELINE configs 3 and 4 shapes) -----------------
+
+@pytest.mark.parametrize("cfg,phi", [(3, 1.0), (4, 1.2)])
+def test_full_size_walk_properties(cfg, phi):
+    p = g9.named_config(cfg, phi)
+    dag, model = g9.instance(p)
+    b = pb.FrontierBatch()
+    b.add(dag, model, g9.TAU)
+    b.run(0)
+    s = b.summary(0)
+    assert s.status == 0 and pb.STOP_NAMES[s.stop] == "at_t_min"
+    assert s.steps == 24 * (p.stages + p.microbatches - 1)
+    pts = b.points(0)
+    tp = pts["t_planned"]
+    assert tp[0] == s.t_star and tp[-1] == s.t_min
+    assert np.all(tp[:-1] - tp[1:] == pts["step_size"][1:])
+    assert np.all(pts["t_realized"] <= tp)
+    # the relaxed energy moves by the cut cost within 1 mJ per touched computation
+    d = np.diff(pts["sum_planned_e"])
+    touched = pts["n_sped"][1:] + pts["n_slowed"][1:]
+    assert np.all(np.abs(d - pts["cut_cost"][1:]) <= touched)
+    # replaying the delta log reproduces the device's running sums
+    last = b.schedule(0, s.steps)
+    assert sum(last.planned_t) == pts["sum_planned_t"][-1]
+    assert sum(last.realized_e) == pts["sum_realized_e"][-1]
