@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark: Perseus frontier generation on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload batch|config1|config2|config3|config4] [--batch 4096]
+                  [--scaling weak|strong]
+
+One "step" = one pass of the hot path over one batch: every instance's full
+frontier walk (frontier.hpp:166-189), one CTA per instance, in one launch of
+the sm_100a walk kernel.  `value` = frontier points/s over the whole job
+(sum over instances of steps + 1, all ranks) with inputs resident in HBM;
+`e2e` = the same metric through the C ABI (pb_batch_run: pack + H2D + walk
+kernel + D2H of the delta-encoded frontiers, host buffers in and out).
+
+Multi-GPU: one process per GPU (torchrun).  Instances are independent, so
+there is no data-path collective: with --scaling weak (default) rank r walks
+instances [r*B, (r+1)*B) of the G9 config-5 sequence; with --scaling strong
+the B instances are LPT-sharded over ranks.  Times are device-measured (CUDA
+events on the walk kernel's stream) and reduced as the max over ranks.
+
+--impl reference runs the UNMODIFIED reference planner (oracle/_ref/ref_driver,
+compiled from /root/reference by `make -C oracle ref`) on the host cores:
+each step is a time-bounded sample of the same batch (see cpu_sample()).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frontier points/sec (min-cut iters/sec) over instance batch at 1/2/4/8 B200 vs CPU"
+UNIT = "frontier points/s"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class Dist:
+    """torch.distributed plumbing (barrier + max-reduce of device times)."""
+
+    def __init__(self, backend="nccl"):
+        self.rank, self.world, self.local = dist_env()
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.dist, self.torch = dist, torch
+            self.dev = torch.device("cuda", self.local) if backend == "nccl" else torch.device("cpu")
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ workload
+
+def batch_indices(batch: int, rank: int, world: int, scaling: str):
+    """Instances of this rank.  weak: its own block of the config-5 sequence;
+    strong: an LPT shard (by estimated work) of instances [0, batch)."""
+    if scaling == "weak":
+        return list(range(rank * batch, (rank + 1) * batch))
+    from paper_2312_06902_b200 import shard
+    return shard.lpt_shard([shard.g9_work_estimate(i) for i in range(batch)], world)[rank]
+
+
+def build_batch(args, rank, world):
+    import paper_2312_06902_b200 as pb
+    from paper_2312_06902_b200 import g9
+    b = pb.FrontierBatch()
+    if args.workload == "batch":
+        idx = batch_indices(args.batch, rank, world, args.scaling)
+        for i in idx:
+            b.add_g9(g9.batch_params(i))
+        desc = (f"G9 config-5 batch: {args.batch} heterogeneous 1F1B instances per "
+                f"{'GPU' if args.scaling == 'weak' else 'job'} (N 4-16, M 8-256, B=10, imbalance 1.0-1.25, "
+                f"straggler phi in 1.0-1.5), full frontiers, tau=1000us")
+        specs = [f"batch:{i}" for i in idx]
+    else:
+        k = int(args.workload[-1])
+        reps = max(1, args.reps)
+        for _ in range(reps):
+            b.add_g9(g9.named_config(k))
+        desc = f"G9 config {k} ({g9.named_config(k).stages}x{g9.named_config(k).microbatches} 1F1B) x{reps}"
+        specs = [f"config:{k}"] * reps
+        idx = list(range(reps))
+    return b, desc, specs, idx
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi sampled DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU side
+
+def ref_driver_path():
+    return os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+
+
+def cpu_sample(specs, budget_s: float, threads: int, stride: int = 256):
+    """The reference planner on a bounded sample of the same batch: every
+    `stride`-th instance (stratified over the mix), each walked from its
+    seed with the reference's public API for at most `budget_s` seconds on
+    its own host thread.  Early steps are the cheapest ones (the critical
+    sub-DAG grows along the walk), so this overstates the reference's
+    throughput -- the reported ratio is conservative."""
+    sample = specs[::stride] if len(specs) > stride else specs[: max(1, threads)]
+    out = subprocess.run([ref_driver_path(), "budget", str(budget_s), str(threads), *sample],
+                         capture_output=True, text=True, check=True)
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    r["sample"] = (f"{len(sample)} instances (every {stride}th of the batch) walked from T* with the "
+                   f"reference API, <= {budget_s:.0f}s each, {threads} threads; "
+                   f"{r['complete']} of them reached T_min")
+    return r
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    if not os.path.exists(ref_driver_path()):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver not built (needs /root/reference)"}))
+        return 0
+    _, desc, specs, _ = build_batch_specs(args)
+    threads = os.cpu_count() or 1
+    budget = args.cpu_budget
+    for _ in range(args.warmup):
+        cpu_sample(specs, min(budget, 2.0), threads)
+    pts = 0
+    wall = 0.0
+    steps = 0
+    last = None
+    for _ in range(args.steps):
+        r = cpu_sample(specs, budget, threads)
+        pts += r["points"]
+        steps += r["steps"]
+        wall += r["wall_s"]
+        last = r
+    value = pts / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (G9 generator, SURVEY.md §8d)",
+        "config": {"workload": desc, "sample": last["sample"]},
+        "iterations_per_s": steps / wall,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": last["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def build_batch_specs(args):
+    from paper_2312_06902_b200 import g9
+    if args.workload == "batch":
+        idx = batch_indices(args.batch, 0, 1, "weak")
+        return None, (f"G9 config-5 batch: {args.batch} heterogeneous 1F1B instances"), [f"batch:{i}" for i in idx], idx
+    k = int(args.workload[-1])
+    return None, f"G9 config {k}", [f"config:{k}"] * max(1, args.reps), None
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def run_ours(args):
+    import paper_2312_06902_b200 as pb  # noqa: F401  (loads the CUDA library; fails loudly if absent)
+    D = Dist("nccl")
+    rank, world = D.rank, D.world
+    device = D.local if world > 1 else 0
+    b, desc, specs, idx = build_batch(args, rank, world)
+    b.prepare(device)
+    # warm-up (untimed)
+    for _ in range(args.warmup):
+        b.launch()
+    D.barrier()
+    kernel_ms = []
+    with ClockSampler(device) as clk:
+        for _ in range(args.steps):
+            D.barrier()
+            kernel_ms.append(b.launch())  # synchronizes its stream on both sides
+            D.barrier()
+    st = b.stats()
+    b.fetch()
+    points = steps = 0
+    bad = 0
+    for k in range(len(b)):
+        s = b.summary(k)
+        bad += s.status != 0
+        points += s.steps + 1
+        steps += s.steps
+    if bad:
+        raise RuntimeError(f"{bad} instances failed on rank {rank}")
+    t_dev = D.max(sum(kernel_ms) / 1e3)
+    total_points = D.sum(points)
+    total_steps = D.sum(steps)
+    value = total_points * args.steps / t_dev
+    # e2e through the C ABI with host buffers: pack + H2D + kernel + D2H
+    e2e_times = []
+    for _ in range(max(1, args.e2e_steps)):
+        D.barrier()
+        t0 = time.perf_counter()
+        b.run(device)
+        _ = [b.summary(k).steps for k in range(len(b))]
+        e2e_times.append(time.perf_counter() - t0)
+        D.barrier()
+    st_e2e = b.stats()
+    t_e2e = D.max(sum(e2e_times))
+    e2e_value = total_points * len(e2e_times) / t_e2e
+    # roofline of the walk kernel: algorithmic bytes from the device counters
+    # (16 B per arc scan, 24 B per node update, 24 B per longest-path visit;
+    # SURVEY.md §8d) over the measured launch time
+    alg_bytes = 16 * st.arc_scans + 24 * st.node_updates + 24 * st.comp_visits
+    launch_s = st.kernel_ms / 1e3
+    peaks = load_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg_bytes / launch_s / 1e9 if launch_s > 0 else 0.0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (G9 generator, SURVEY.md §8d)",
+        "config": {"workload": desc, "instances_per_rank": len(b), "tau_us": 1000,
+                   "l2": "working set > 126 MB L2 (instance data + per-CTA residual state); no flush",
+                   "parallelism": f"instances sharded over {world} GPU(s), one CTA per instance"},
+        "iterations_per_s": total_steps * args.steps / t_dev,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(st_e2e.h2d_bytes),
+                "d2h_bytes_per_step": int(st_e2e.d2h_bytes)},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "counters": {"arc_scans": st.arc_scans, "node_updates": st.node_updates,
+                                  "comp_visits": st.comp_visits, "rounds": st.rounds},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu and os.path.exists(ref_driver_path()):
+        r = cpu_sample(specs, args.cpu_budget, os.cpu_count() or 1)
+        line["cpu_baseline"] = {"value": r["points"] / r["wall_s"], "unit": UNIT, "cores": r["threads"],
+                                "kind": "reference", "sample": r["sample"]}
+    if rank == 0:
+        print(json.dumps(line))
+    D.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="batch",
+                    choices=["batch", "config1", "config2", "config3", "config4"])
+    ap.add_argument("--batch", type=int, default=4096)
+    ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

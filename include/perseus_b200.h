@@ -35,8 +35,8 @@ typedef enum {
   PB_ERR_LOGIC = 3,            /* std::logic_error (flow.hpp:265; frontier.hpp:213) */
   PB_ERR_DOMAIN = 4,           /* DegenerateFit, std::domain_error (costmodel.hpp:50-52) */
   PB_ERR_CUDA = 5,             /* device failure (no reference counterpart) */
-  PB_ERR_UNSUPPORTED = 6       /* documented divergence: a curve evaluated outside
-                                  its profiled interval (SURVEY.md §7 parity rule 5) */
+  PB_ERR_UNSUPPORTED = 6       /* input outside what the device layout supports
+                                  (e.g. a curve interval too long to tabulate) */
 } pb_status;
 
 /* Why a frontier walk ended (frontier.hpp:178-187). */
@@ -102,6 +102,11 @@ typedef struct {
   int32_t stop;   /* pb_stop_reason */
   int32_t status; /* pb_status of this instance */
   int32_t n_ids;  /* total delta records */
+  /* curve evaluations outside [t_min, t_max] (done with device exp instead
+   * of the host table; the reference evaluates the curve there too,
+   * costmodel.hpp:47).  0 on every G9 and golden walk. */
+  int32_t n_extrapolated;
+  int32_t pad;
 } pb_frontier_summary;
 
 /* Per-point scalars; point 0 is the T* seed, point k>0 follows step k. */
@@ -172,6 +177,7 @@ typedef struct {
   int64_t node_updates;
   int64_t rounds;
   int64_t kernel_launches;
+  int64_t comp_visits; /* longest-path node visits */
 } pb_run_stats;
 pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out);
 void pb_batch_destroy(pb_batch* b);
@@ -205,6 +211,11 @@ pb_status pb_g9_stage_bases(int32_t stages, int32_t base, double imbalance, uint
 pb_status pb_g9_batch_params(int32_t i, int32_t* stages, int32_t* microbatches,
                              double* imbalance, double* phi, int32_t* straggler,
                              uint32_t* seed);
+/* Appends a complete G9 instance (1F1B DAG, build_pipeline dag.hpp:112-143;
+ * G9 profiles; CostModel::build with pareto_filter + fit_exp) to a batch. */
+pb_status pb_batch_add_g9(pb_batch* b, int32_t stages, int32_t microbatches, int32_t base,
+                          double imbalance, uint32_t seed, int32_t straggler_stage, double phi,
+                          int64_t tau, int32_t* out_index);
 /* The 9 (freq, time, energy) points of a stage base (descending frequency). */
 pb_status pb_g9_profile(int32_t b, int32_t backward, int64_t tau, int32_t* freq, int64_t* time,
                         int64_t* energy);

@@ -497,6 +497,61 @@ int mode_bench(int argc, char** argv) {
   return 0;
 }
 
+// Time-bounded walks: every instance walks from its seed with the
+// reference's public API (the discover_frontier loop, frontier.hpp:166-189)
+// until it reaches T_min or its per-instance budget expires; instances run
+// one per thread.  Frontier points = schedules produced (seed included).
+int mode_budget(int argc, char** argv) {
+  const double budget = std::stod(argv[2]);
+  const int threads = std::max(1, std::stoi(argv[3]));
+  std::vector<std::string> specs;
+  for (int i = 4; i < argc; ++i) specs.push_back(argv[i]);
+  std::vector<Instance> insts;
+  for (const auto& s : specs) insts.push_back(make_instance(s));
+  std::atomic<size_t> next{0};
+  std::atomic<long long> points{0}, steps{0}, complete{0};
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&] {
+      for (;;) {
+        const size_t i = next.fetch_add(1);
+        if (i >= insts.size()) return;
+        const Instance& in = insts[i];
+        const auto s0 = std::chrono::steady_clock::now();
+        const AllMaxAssignment am = all_max_assignment(in.dag, in.model);
+        const Quanta t_min = simulate(in.dag, am.durations).iteration_time;
+        EnergySchedule cur = min_energy_schedule(in.dag, in.model);
+        EnergySchedule first = discretize(cur, in.dag, in.model);
+        long long p = 1, k = 0;
+        bool done = true;
+        while (cur.t_planned > t_min) {
+          if (std::chrono::duration<double>(std::chrono::steady_clock::now() - s0).count() > budget) {
+            done = false;
+            break;
+          }
+          const Quanta step = std::min<Quanta>(in.tau, cur.t_planned - t_min);
+          auto nxt = get_next_schedule(in.dag, cur, in.model, step);
+          if (!nxt || nxt->t_planned >= cur.t_planned) break;
+          cur = std::move(*nxt);
+          EnergySchedule d = discretize(cur, in.dag, in.model);
+          ++p;
+          ++k;
+        }
+        points += p;
+        steps += k;
+        if (done) ++complete;
+      }
+    });
+  for (auto& th : pool) th.join();
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::printf("{\"instances\":%zu,\"threads\":%d,\"budget_s\":%.3f,\"points\":%lld,\"steps\":%lld,"
+              "\"complete\":%lld,\"wall_s\":%.6f}\n",
+              insts.size(), threads, budget, points.load(), steps.load(), complete.load(), wall);
+  (void)argc;
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -517,6 +572,7 @@ int main(int argc, char** argv) {
     if (mode == "flow") return mode_flow(argc, argv);
     if (mode == "slack") return mode_slack(argc, argv);
     if (mode == "bench") return mode_bench(argc, argv);
+    if (mode == "budget") return mode_budget(argc, argv);
     if (mode == "fit") {
       for (int i = 2; i < argc; ++i) {
         const Instance in = make_instance(argv[i]);

@@ -92,6 +92,8 @@ class FrontierSummary(C.Structure):
         ("stop", C.c_int32),
         ("status", C.c_int32),
         ("n_ids", C.c_int32),
+        ("n_extrapolated", C.c_int32),
+        ("pad", C.c_int32),
     ]
 
 
@@ -123,6 +125,7 @@ class RunStats(C.Structure):
         ("node_updates", C.c_int64),
         ("rounds", C.c_int64),
         ("kernel_launches", C.c_int64),
+        ("comp_visits", C.c_int64),
     ]
 
 
@@ -160,6 +163,8 @@ def _load() -> C.CDLL:
                                         C.c_double, i32p]),
         "pb_g9_batch_params": (C.c_int, [C.c_int32, i32p, i32p, f64p, f64p, i32p, C.POINTER(C.c_uint32)]),
         "pb_g9_profile": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, i32p, i64p, i64p]),
+        "pb_batch_add_g9": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_uint32, C.c_int32,
+                                      C.c_double, C.c_int64, i32p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -176,7 +181,7 @@ EXPORTED = (
     "pb_batch_run", "pb_batch_prepare", "pb_batch_launch", "pb_batch_fetch", "pb_batch_size",
     "pb_batch_run_multi", "pb_batch_summary", "pb_batch_points", "pb_batch_deltas", "pb_batch_schedule",
     "pb_batch_stats", "pb_batch_destroy", "pb_annotate_slack_batch", "pb_flow_min_cut_batch",
-    "pb_g9_stage_bases", "pb_g9_batch_params", "pb_g9_profile",
+    "pb_g9_stage_bases", "pb_g9_batch_params", "pb_g9_profile", "pb_batch_add_g9",
 )
 
 

@@ -307,7 +307,7 @@ struct Packed {
 enum OffIdx {
   O_CLASS, O_LVLOFF, O_LVL, O_INOFF, O_INDEP, O_OUTOFF, O_OUTDEP, O_SNK, O_DTAIL, O_DHEAD,
   O_INCOFF, O_INC, O_ECT, O_ECH, O_CCONST, O_CTMIN, O_CTMAX, O_CTAB, O_CPOFF, O_PTIME, O_PENERGY,
-  O_START, O_POINTS, O_IDS, O_CHOICE, O_SUMMARY, O_COUNT
+  O_START, O_CURVE, O_POINTS, O_IDS, O_CHOICE, O_SUMMARY, O_COUNT
 };
 
 void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, std::vector<int32_t>& cap_ids,
@@ -382,6 +382,7 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, std::vector<
     o[O_PTIME] = P.stat.put(h.pt_time);
     o[O_PENERGY] = P.stat.put(h.pt_energy);
     o[O_START] = h.start.empty() ? SIZE_MAX : P.stat.put(h.start);
+    o[O_CURVE] = P.stat.put(h.cls_curve);
     const int64_t est = static_cast<int64_t>(static_cast<double>(h.est_steps) * cap_scale);
     cap_points[k] = static_cast<int32_t>(std::min<int64_t>(est + 8, INT32_MAX / 2));
     cap_ids[k] = static_cast<int32_t>(std::min<int64_t>(est * 8 + 2 * int64_t{h.n} + 64, INT32_MAX / 2));
@@ -459,6 +460,7 @@ void bind_device(Packed& P, char* d_static, char* d_out, size_t tables_off) {
     d.pt_energy = dptr<int64_t>(d_static, o[O_PENERGY]);
     d.tables = dptr<double>(d_static, tables_off);
     d.start_planned_t = dptr<int64_t>(d_static, o[O_START]);
+    d.cls_curve = dptr<double>(d_static, o[O_CURVE]);
     d.points = dptr<pb_point>(d_out, o[O_POINTS]);
     d.ids = dptr<int32_t>(d_out, o[O_IDS]);
     d.choice = dptr<uint8_t>(d_out, o[O_CHOICE]);
@@ -551,6 +553,7 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   b->stats.arc_scans = static_cast<int64_t>(rcnt.arc_scans);
   b->stats.node_updates = static_cast<int64_t>(rcnt.node_updates);
   b->stats.rounds = static_cast<int64_t>(rcnt.rounds);
+  b->stats.comp_visits = static_cast<int64_t>(rcnt.comp_visits);
   b->stats.kernel_launches += 1;
   if (kernel_ms) *kernel_ms = ms;
   return PB_OK;
@@ -836,6 +839,7 @@ pb_status pb_batch_run_multi(pb_batch* b, int32_t n_devices, const int32_t* devi
       b->stats.arc_scans += s.stats.arc_scans;
       b->stats.node_updates += s.stats.node_updates;
       b->stats.rounds += s.stats.rounds;
+      b->stats.comp_visits += s.stats.comp_visits;
       b->stats.kernel_launches += s.stats.kernel_launches;
     }
     b->out = std::move(out);
@@ -1210,6 +1214,121 @@ pb_status pb_g9_batch_params(int32_t i, int32_t* stages, int32_t* microbatches, 
   *straggler = p.straggler_stage;
   *seed = p.seed;
   return PB_OK;
+}
+
+pb_status pb_batch_add_g9(pb_batch* b, int32_t stages, int32_t microbatches, int32_t base,
+                          double imbalance, uint32_t seed, int32_t straggler_stage, double phi,
+                          int64_t tau, int32_t* out_index) {
+  if (!b) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
+  if (stages < 1) return fail(PB_ERR_INVALID_ARGUMENT, "pipeline needs at least one stage");
+  if (microbatches < 1) return fail(PB_ERR_INVALID_ARGUMENT, "pipeline needs at least one microbatch");
+  pb_g9::Params p;
+  p.stages = stages;
+  p.microbatches = microbatches;
+  p.base = base;
+  p.imbalance = imbalance;
+  p.seed = seed;
+  p.straggler_stage = straggler_stage;
+  p.phi = phi;
+  const auto bases = pb_g9::stage_bases(p);
+  // build_pipeline (dag.hpp:112-143), 1F1B stage streams (dag.hpp:91-103):
+  // ids stage-major in stream order; kind 0 forward, 1 backward.
+  const int32_t N = stages, M = microbatches, n = 2 * N * M;
+  std::vector<int32_t> comp_class(n), fid(N * M), bid(N * M);
+  std::vector<std::vector<int32_t>> order(N);
+  int32_t id = 0;
+  for (int32_t s = 0; s < N; ++s) {
+    const int32_t warm = std::min(M, N - s);
+    int32_t f = 0, bw = 0;
+    auto emit = [&](int kind, int32_t m) {
+      comp_class[id] = 2 * s + kind;  // classes sorted by (stage, kind)
+      (kind == 0 ? fid : bid)[s * M + m] = id;
+      order[s].push_back(id++);
+    };
+    for (; f < warm; ++f) emit(0, f);
+    while (f < M) {
+      emit(1, bw++);
+      emit(0, f++);
+    }
+    while (bw < M) emit(1, bw++);
+  }
+  std::vector<int32_t> et, eh;
+  for (int32_t s = 0; s < N; ++s)
+    for (size_t i = 0; i + 1 < order[s].size(); ++i) {
+      et.push_back(order[s][i]);
+      eh.push_back(order[s][i + 1]);
+    }
+  for (int32_t s = 0; s + 1 < N; ++s)
+    for (int32_t m = 0; m < M; ++m) {
+      et.push_back(fid[s * M + m]);
+      eh.push_back(fid[(s + 1) * M + m]);
+      et.push_back(bid[(s + 1) * M + m]);
+      eh.push_back(bid[s * M + m]);
+    }
+  for (int32_t s = 0; s < N; ++s) {
+    et.push_back(n);
+    eh.push_back(order[s].front());
+    et.push_back(order[s].back());
+    eh.push_back(n + 1);
+  }
+  // CostModel::build (costmodel.hpp:215-238) over the 2N G9 classes
+  std::vector<uint8_t> cconst(2 * N, 0);
+  std::vector<int32_t> poff{0}, pf;
+  std::vector<int64_t> pt, pe, trange(4 * N);
+  std::vector<double> curve(6 * N);
+  for (int32_t s = 0; s < N; ++s)
+    for (int kind = 0; kind < 2; ++kind) {
+      const auto raw = pb_g9::stage_profile(bases[s], kind == 1, pb_g9::kTau);
+      const int32_t c = 2 * s + kind;
+      std::vector<int32_t> f(raw.size()), of(raw.size());
+      std::vector<int64_t> t(raw.size()), e(raw.size()), ot(raw.size()), oe(raw.size());
+      for (size_t j = 0; j < raw.size(); ++j) {
+        f[j] = raw[j].freq_mhz;
+        t[j] = raw[j].time;
+        e[j] = raw[j].energy;
+      }
+      const int32_t k = pb_pareto_filter(static_cast<int32_t>(raw.size()), f.data(), t.data(), e.data(),
+                                         of.data(), ot.data(), oe.data());
+      double abcr[4] = {0, 0, 0, 0};
+      if (k == 1 || pb_fit_exp(k, ot.data(), oe.data(), abcr) != PB_OK) {
+        cconst[c] = 1;
+        pf.push_back(of[0]);
+        pt.push_back(ot[0]);
+        pe.push_back(oe[0]);
+      } else {
+        for (int32_t j = 0; j < k; ++j) {
+          pf.push_back(of[j]);
+          pt.push_back(ot[j]);
+          pe.push_back(oe[j]);
+        }
+        curve[3 * c] = abcr[0];
+        curve[3 * c + 1] = abcr[1];
+        curve[3 * c + 2] = abcr[2];
+        trange[2 * c] = ot[0];
+        trange[2 * c + 1] = ot[k - 1];
+      }
+      poff.push_back(static_cast<int32_t>(pt.size()));
+    }
+  pb_instance_desc d{};
+  d.n = n;
+  d.comp_class = comp_class.data();
+  d.n_edges = static_cast<int32_t>(et.size());
+  d.edge_tail = et.data();
+  d.edge_head = eh.data();
+  d.n_classes = 2 * N;
+  d.class_is_constant = cconst.data();
+  d.class_point_off = poff.data();
+  d.point_freq = pf.data();
+  d.point_time = pt.data();
+  d.point_energy = pe.data();
+  d.class_curve = curve.data();
+  d.class_t_range = trange.data();
+  d.blocking_watts = 75.0;
+  d.quantum_us = 1;
+  d.tau = tau;
+  d.start_planned_t = nullptr;
+  d.max_steps = 0;
+  return pb_batch_add(b, &d, out_index);
 }
 
 pb_status pb_g9_profile(int32_t b, int32_t backward, int64_t tau, int32_t* freq, int64_t* time,

@@ -51,6 +51,7 @@ struct DevInst {
   const int64_t* pt_time;
   const int64_t* pt_energy;
   const double* tables;           // E(t) = a exp(b t) + c for t in [t_min, t_max]
+  const double* cls_curve;        // [3 * classes] a, b, c (extrapolation only)
   const int64_t* start_planned_t; // get-next mode only
   // outputs
   pb_point* points;             // [cap_points]

@@ -567,19 +567,20 @@ __device__ __forceinline__ int discretize_choice(const DevInst& I, int c, long l
   return chosen;
 }
 
-// planned_energy (frontier.hpp:59-62) from the host table; *bad on a lookup
-// outside [t_min, t_max].
-__device__ __forceinline__ long long table_energy(const DevInst& I, int c, long long t, int* bad) {
-  if (I.cls_const[c]) return I.pt_energy[I.cls_pt_off[c]];
-  if (t < I.cls_tmin[c] || t > I.cls_tmax[c]) {
-    *bad = 1;
-    return 0;
-  }
-  return llround(I.tables[I.cls_tab[c] + (t - I.cls_tmin[c])]);
+// ExpCurve::eval (costmodel.hpp:47) from the host table (bit-identical to the
+// reference's libm values); outside [t_min, t_max] -- reachable only from a
+// caller-supplied start schedule or the infinite-edge cut case (SURVEY.md §7
+// parity rule 5) -- the device evaluates the curve itself and counts it.
+__device__ __forceinline__ double table_at(const DevInst& I, int c, long long t, int* extrap) {
+  if (t >= I.cls_tmin[c] && t <= I.cls_tmax[c]) return I.tables[I.cls_tab[c] + (t - I.cls_tmin[c])];
+  ++*extrap;
+  return I.cls_curve[3 * c] * exp(I.cls_curve[3 * c + 1] * static_cast<double>(t)) + I.cls_curve[3 * c + 2];
 }
 
-__device__ __forceinline__ double table_at(const DevInst& I, int c, long long t) {
-  return I.tables[I.cls_tab[c] + (t - I.cls_tmin[c])];
+// planned_energy (frontier.hpp:59-62).
+__device__ __forceinline__ long long table_energy(const DevInst& I, int c, long long t, int* extrap) {
+  if (I.cls_const[c]) return I.pt_energy[I.cls_pt_off[c]];
+  return llround(table_at(I, c, t, extrap));
 }
 
 __device__ void write_point(const DevInst& I, int k, long long tp, long long tr, long long spe,
@@ -659,10 +660,6 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, Sh& sh, Counters& C)
   spt = block_reduce(spt, sh, OpSum(), 0);
   sre = block_reduce(sre, sh, OpSum(), 0);
   srt = block_reduce(srt, sh, OpSum(), 0);
-  if (block_reduce(bad, sh, OpMax(), 0)) {
-    if (tid == 0) I.summary->status = PB_ERR_UNSUPPORTED;
-    return;
-  }
 
   const long long t_min = forward_pass(I, W.pdur, W.estart, sh, C);
   long long t_cur = forward_pass(I, W.planned, W.estart, sh, C);
@@ -704,7 +701,6 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, Sh& sh, Counters& C)
     __syncthreads();
     i128 suml = 0, sumu = 0;
     long long ninf = 0;
-    int bad_l = 0;
     for (int i = tid; i < n; i += kBlock) {
       const int c = I.comp_class[i];
       const long long t = W.planned[i];
@@ -715,19 +711,15 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, Sh& sh, Counters& C)
         const long long tmin = I.cls_tmin[c], tmax = I.cls_tmax[c];
         const bool can_speed = t - step >= tmin;
         const bool can_slow = t + step <= tmax;
-        if ((can_speed || can_slow) && (t < tmin || t > tmax)) {
-          bad_l = 1;
-        } else {
-          const double et = (can_speed || can_slow) ? table_at(I, c, t) : 0.0;
-          if (can_slow) {
-            const long long r = llround(et - table_at(I, c, t + step));
-            l = r > 0 ? r : 0;
-          }
-          if (can_speed) {
-            const long long r = llround(table_at(I, c, t - step) - et);
-            capv = (r > l ? r : l) - l;
-            inf = 0;
-          }
+        const double et = (can_speed || can_slow) ? table_at(I, c, t, &bad) : 0.0;
+        if (can_slow) {
+          const long long r = llround(et - table_at(I, c, t + step, &bad));
+          l = r > 0 ? r : 0;
+        }
+        if (can_speed) {
+          const long long r = llround(table_at(I, c, t - step, &bad) - et);
+          capv = (r > l ? r : l) - l;
+          inf = 0;
         }
       }
       N.ecrit[i] = crit;
@@ -783,10 +775,6 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, Sh& sh, Counters& C)
       N.einf[N.ret] = 0;
       N.cap[N.ret] = 0;
       N.flow[N.ret] = 0;
-    }
-    if (block_reduce(bad_l, sh, OpMax(), 0)) {
-      status = PB_ERR_UNSUPPORTED;
-      break;
     }
     suml = block_sum128(suml, sh);
     sumu = block_sum128(sumu, sh);
@@ -856,7 +844,6 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, Sh& sh, Counters& C)
     // order: sped ascending, then slowed ascending (frontier.hpp:111-125)
     int ns_loc = 0;
     long long dpe = 0, dpt = 0, dre = 0, drt = 0;
-    int bad_u = 0;
     for (int q = tid; q < nd; q += kBlock) {
       const int x = W.delta[q];
       const long long kx = x > 0 ? x : (1ll << 40) - x;
@@ -870,8 +857,8 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, Sh& sh, Counters& C)
       const int c = I.comp_class[i];
       const long long told = W.planned[i];
       const long long tnew = x > 0 ? told - step : told + step;
-      const long long eold = table_energy(I, c, told, &bad_u);
-      const long long enew = table_energy(I, c, tnew, &bad_u);
+      const long long eold = table_energy(I, c, told, &bad);
+      const long long enew = table_energy(I, c, tnew, &bad);
       const int chold = W.choice[i];
       const int chnew = discretize_choice(I, c, tnew);
       const int p0 = I.cls_pt_off[c];
@@ -900,10 +887,6 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, Sh& sh, Counters& C)
     dpt = block_reduce(dpt, sh, OpSum(), 0);
     dre = block_reduce(dre, sh, OpSum(), 0);
     drt = block_reduce(drt, sh, OpSum(), 0);
-    if (block_reduce(bad_u, sh, OpMax(), 0)) {
-      status = PB_ERR_UNSUPPORTED;
-      break;
-    }
     // refresh_totals (frontier.hpp:64-67): new planned makespan
     const long long t_new = forward_pass(I, W.planned, W.estart, sh, C);
     if (I.mode == kModeDiscover && t_new >= t_cur) {
@@ -921,15 +904,17 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, Sh& sh, Counters& C)
     if (tid == 0) write_point(I, steps, t_cur, t_real, spe, spt, sre, srt, cost, step, id_total, ns, nd - ns);
     id_total += nd;
   }
-  __syncthreads();
+  const long long n_extrap = block_reduce(bad, sh, OpSum(), 0);
   if (tid == 0) {
     pb_frontier_summary s;
+    s.n_extrapolated = static_cast<int32_t>(n_extrap);
     s.t_min = t_min;
     s.t_star = t_star;
     s.steps = steps;
     s.stop = stop;
     s.status = status;
     s.n_ids = id_total;
+    s.pad = 0;
     *I.summary = s;
   }
   __syncthreads();

@@ -56,6 +56,11 @@ class StepInfo:
     slowed_down: List[int] = field(default_factory=list)
 
 
+class _G9Meta:
+    def __init__(self, n: int):
+        self.n = n
+
+
 class FrontierBatch:
     """A batch of independent frontier walks on one device (pb_batch)."""
 
@@ -83,6 +88,14 @@ class FrontierBatch:
         idx = C.c_int32()
         N.check(N.lib.pb_batch_add(self._h, C.byref(p.desc), C.byref(idx)))
         self._packed.append(p)
+        return idx.value
+
+    def add_g9(self, p, tau: int = 1000) -> int:
+        """Appends a G9 instance built natively (pb_batch_add_g9)."""
+        idx = C.c_int32()
+        N.check(N.lib.pb_batch_add_g9(self._h, p.stages, p.microbatches, p.base, p.imbalance, p.seed,
+                                      p.straggler_stage, p.phi, tau, C.byref(idx)))
+        self._packed.append(_G9Meta(2 * p.stages * p.microbatches))
         return idx.value
 
     def add_packed(self, p: PackedInstance) -> int:
