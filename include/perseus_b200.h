@@ -180,6 +180,11 @@ typedef struct {
   int64_t comp_visits; /* longest-path node visits */
 } pb_run_stats;
 pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out);
+/* Raw per-phase profile of the last launch (cycles summed over CTAs, then
+ * counts), n <= 16 slots: LP, capacities, phase A, phase B, global relabel,
+ * cut BFS, update, whole walk, GR calls, GR levels, cut levels, rounds A,
+ * rounds B, steps, max rounds of one push-relabel call, LP levels. */
+pb_status pb_batch_profile(const pb_batch* b, int64_t* out, int32_t n);
 void pb_batch_destroy(pb_batch* b);
 
 /* ---- component kernels, exposed for parity tests ----------------------- */

@@ -250,6 +250,10 @@ struct DeviceRun {
   int32_t* d_order = nullptr;
   int32_t* d_counter = nullptr;
   pb::RunCounters* d_counters = nullptr;
+  int32_t* d_pool_ids = nullptr;
+  uint8_t* d_pool_choice = nullptr;
+  unsigned long long* d_pool_cursor = nullptr;
+  long long pool_cap = 0;
   size_t out_bytes = 0;
   int32_t slots = 0;
   pb::WsLayout ws{};
@@ -266,6 +270,9 @@ struct DeviceRun {
     cudaFree(d_order);
     cudaFree(d_counter);
     cudaFree(d_counters);
+    cudaFree(d_pool_ids);
+    cudaFree(d_pool_choice);
+    cudaFree(d_pool_cursor);
     if (h_out) cudaFreeHost(h_out);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -282,12 +289,17 @@ struct pb_batch {
   std::vector<double> tables;
   std::vector<std::vector<int64_t>> cls_tab;  // per instance per class
   // outputs (host copies)
-  std::vector<size_t> out_points, out_ids, out_choice, out_summary;
-  std::vector<int32_t> cap_points, cap_ids;
-  std::vector<char> out;  // host results
+  std::vector<size_t> out_points, out_summary;
+  std::vector<int32_t> cap_points;
+  std::vector<char> out;  // host results: points + summaries
+  std::vector<int32_t> pool_ids;  // delta pool (used prefix)
+  std::vector<uint8_t> pool_choice;
+  std::vector<long long> pool_base;  // per instance: offset of its id_begin values
+  long long pool_cap = 0;
   bool have_results = false;
   DeviceRun run;
   pb_run_stats stats{};
+  int64_t prof[pb::kPrSlots] = {};
   ~pb_batch() { run.release(); }
 };
 
@@ -296,6 +308,7 @@ namespace {
 // Packs all instances; returns host blobs and per-instance DevInst with
 // offsets (converted to device pointers once the blob is uploaded).
 struct Packed {
+  long long pool_cap = 0;
   Blob stat;
   std::vector<pb::DevInst> dev;
   std::vector<std::array<size_t, 32>> offs;
@@ -307,11 +320,10 @@ struct Packed {
 enum OffIdx {
   O_CLASS, O_LVLOFF, O_LVL, O_INOFF, O_INDEP, O_OUTOFF, O_OUTDEP, O_SNK, O_DTAIL, O_DHEAD,
   O_INCOFF, O_INC, O_ECT, O_ECH, O_CCONST, O_CTMIN, O_CTMAX, O_CTAB, O_CPOFF, O_PTIME, O_PENERGY,
-  O_START, O_CURVE, O_POINTS, O_IDS, O_CHOICE, O_SUMMARY, O_COUNT
+  O_START, O_CURVE, O_POINTS, O_SUMMARY, O_COUNT
 };
 
-void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, std::vector<int32_t>& cap_ids,
-          double cap_scale) {
+void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_scale) {
   const size_t N = b->insts.size();
   // curve tables, deduplicated by (a, b, c, t_min, t_max) bit patterns
   std::map<CurveKey, int64_t> table_of;
@@ -344,7 +356,7 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, std::vector<
   P.dev.assign(N, pb::DevInst{});
   P.offs.assign(N, {});
   cap_points.assign(N, 0);
-  cap_ids.assign(N, 0);
+  long long pool = 0;
   size_t out = 0;
   auto out_take = [&](size_t bytes) {
     const size_t at = (out + 255) / 256 * 256;
@@ -385,10 +397,8 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, std::vector<
     o[O_CURVE] = P.stat.put(h.cls_curve);
     const int64_t est = static_cast<int64_t>(static_cast<double>(h.est_steps) * cap_scale);
     cap_points[k] = static_cast<int32_t>(std::min<int64_t>(est + 8, INT32_MAX / 2));
-    cap_ids[k] = static_cast<int32_t>(std::min<int64_t>(est * 8 + 2 * int64_t{h.n} + 64, INT32_MAX / 2));
+    pool += est * 12 + 2 * int64_t{h.n} + 64;
     o[O_POINTS] = out_take(sizeof(pb_point) * cap_points[k]);
-    o[O_IDS] = out_take(sizeof(int32_t) * cap_ids[k]);
-    o[O_CHOICE] = out_take(cap_ids[k]);
     o[O_SUMMARY] = out_take(sizeof(pb_frontier_summary));
     pb::DevInst& d = P.dev[k];
     d.n = h.n;
@@ -397,7 +407,7 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, std::vector<
     d.mode = h.start.empty() ? pb::kModeDiscover : pb::kModeGetNext;
     d.max_steps = h.start.empty() ? h.max_steps : (h.max_steps == 0 ? 1 : h.max_steps);
     d.cap_points = cap_points[k];
-    d.cap_ids = cap_ids[k];
+    d.cap_ids = 0;
     d.tau = h.tau;
     d.watts = h.watts;
     d.quantum = h.quantum;
@@ -407,6 +417,7 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, std::vector<
     P.max_e = std::max<int64_t>(P.max_e, h.n + static_cast<int64_t>(h.edge_tail.size()) + 1);
   }
   P.out_bytes = out;
+  P.pool_cap = std::min<long long>(pool, (1ll << 31) - 1);
   (void)tables_off;
   // LPT: largest estimated work first
   P.order.resize(N);
@@ -415,15 +426,12 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, std::vector<
     return b->insts[x].work > b->insts[y].work;
   });
   b->cap_points = cap_points;
-  b->cap_ids = cap_ids;
+  b->pool_cap = P.pool_cap;
   b->out_points.assign(N, 0);
-  b->out_ids.assign(N, 0);
-  b->out_choice.assign(N, 0);
   b->out_summary.assign(N, 0);
+  b->pool_base.assign(N, 0);
   for (size_t k = 0; k < N; ++k) {
     b->out_points[k] = P.offs[k][O_POINTS];
-    b->out_ids[k] = P.offs[k][O_IDS];
-    b->out_choice[k] = P.offs[k][O_CHOICE];
     b->out_summary[k] = P.offs[k][O_SUMMARY];
   }
 }
@@ -462,8 +470,6 @@ void bind_device(Packed& P, char* d_static, char* d_out, size_t tables_off) {
     d.start_planned_t = dptr<int64_t>(d_static, o[O_START]);
     d.cls_curve = dptr<double>(d_static, o[O_CURVE]);
     d.points = dptr<pb_point>(d_out, o[O_POINTS]);
-    d.ids = dptr<int32_t>(d_out, o[O_IDS]);
-    d.choice = dptr<uint8_t>(d_out, o[O_CHOICE]);
     d.summary = dptr<pb_frontier_summary>(d_out, o[O_SUMMARY]);
   }
 }
@@ -484,8 +490,8 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   ck(cudaSetDevice(device), "cudaSetDevice");
   R.device = device;
   Packed P;
-  std::vector<int32_t> capp, capi;
-  pack(b, P, capp, capi, cap_scale);
+  std::vector<int32_t> capp;
+  pack(b, P, capp, cap_scale);
   const size_t tables_off = 0;  // tables are the first section of the blob
   ck(cudaStreamCreateWithFlags(&R.stream, cudaStreamNonBlocking), "stream");
   ck(cudaEventCreate(&R.ev0), "event");
@@ -505,6 +511,10 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   ck(cudaMalloc(&R.d_order, sizeof(int32_t) * N), "malloc order");
   ck(cudaMalloc(&R.d_counter, sizeof(int32_t)), "malloc counter");
   ck(cudaMalloc(&R.d_counters, sizeof(pb::RunCounters)), "malloc counters");
+  R.pool_cap = P.pool_cap;
+  ck(cudaMalloc(&R.d_pool_ids, sizeof(int32_t) * std::max<long long>(R.pool_cap, 1)), "malloc pool");
+  ck(cudaMalloc(&R.d_pool_choice, std::max<long long>(R.pool_cap, 1)), "malloc pool");
+  ck(cudaMalloc(&R.d_pool_cursor, sizeof(unsigned long long)), "malloc cursor");
   ck(cudaEventRecord(h0, R.stream), "record");
   ck(cudaMemcpyAsync(R.d_static, P.stat.bytes.data(), P.stat.bytes.size(), cudaMemcpyHostToDevice,
                      R.stream),
@@ -539,9 +549,11 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   ck(cudaSetDevice(R.device), "cudaSetDevice");
   ck(cudaMemsetAsync(R.d_counter, 0, sizeof(int32_t), R.stream), "memset");
   ck(cudaMemsetAsync(R.d_counters, 0, sizeof(pb::RunCounters), R.stream), "memset");
+  ck(cudaMemsetAsync(R.d_pool_cursor, 0, sizeof(unsigned long long), R.stream), "memset");
+  pb::DeltaPool pool{R.d_pool_ids, R.d_pool_choice, R.d_pool_cursor, R.pool_cap};
   ck(cudaEventRecord(R.ev0, R.stream), "record");
   const int rc = pb::launch_walks(R.d_insts, static_cast<int32_t>(N), R.d_order, R.d_counter,
-                                  R.d_ws, R.ws, R.slots, R.d_counters, R.stream);
+                                  R.d_ws, R.ws, R.slots, R.d_counters, pool, R.stream);
   if (rc != 0) throw CudaError(std::string("walk launch: ") + cudaGetErrorString(static_cast<cudaError_t>(rc)));
   ck(cudaEventRecord(R.ev1, R.stream), "record");
   ck(cudaStreamSynchronize(R.stream), "walk kernel");
@@ -554,6 +566,7 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   b->stats.node_updates = static_cast<int64_t>(rcnt.node_updates);
   b->stats.rounds = static_cast<int64_t>(rcnt.rounds);
   b->stats.comp_visits = static_cast<int64_t>(rcnt.comp_visits);
+  for (int q = 0; q < pb::kPrSlots; ++q) b->prof[q] = static_cast<int64_t>(rcnt.prof[q]);
   b->stats.kernel_launches += 1;
   if (kernel_ms) *kernel_ms = ms;
   return PB_OK;
@@ -571,6 +584,19 @@ pb_status fetch_impl(pb_batch* b) {
   ck(cudaEventCreate(&e1), "event");
   ck(cudaEventRecord(e0, R.stream), "record");
   ck(cudaMemcpyAsync(R.h_out, R.d_out, R.out_bytes, cudaMemcpyDeviceToHost, R.stream), "D2H out");
+  unsigned long long used = 0;
+  ck(cudaMemcpyAsync(&used, R.d_pool_cursor, sizeof used, cudaMemcpyDeviceToHost, R.stream), "D2H cursor");
+  ck(cudaStreamSynchronize(R.stream), "sync");
+  const long long nused = std::min<long long>(static_cast<long long>(used), R.pool_cap);
+  b->pool_ids.resize(nused);
+  b->pool_choice.resize(nused);
+  if (nused) {
+    ck(cudaMemcpyAsync(b->pool_ids.data(), R.d_pool_ids, sizeof(int32_t) * nused, cudaMemcpyDeviceToHost,
+                       R.stream),
+       "D2H pool");
+    ck(cudaMemcpyAsync(b->pool_choice.data(), R.d_pool_choice, nused, cudaMemcpyDeviceToHost, R.stream),
+       "D2H pool");
+  }
   ck(cudaEventRecord(e1, R.stream), "record");
   ck(cudaStreamSynchronize(R.stream), "sync");
   float ms = 0;
@@ -579,7 +605,7 @@ pb_status fetch_impl(pb_batch* b) {
   cudaEventDestroy(e1);
   b->out.assign(R.h_out, R.h_out + R.out_bytes);
   b->stats.d2h_ms = ms;
-  b->stats.d2h_bytes = static_cast<int64_t>(R.out_bytes);
+  b->stats.d2h_bytes = static_cast<int64_t>(R.out_bytes + 5 * nused + sizeof used);
   b->have_results = true;
   return PB_OK;
 }
@@ -808,28 +834,29 @@ pb_status pb_batch_run_multi(pb_batch* b, int32_t n_devices, const int32_t* devi
     b->run.release();
     std::vector<char> out;
     b->out_points.assign(N, 0);
-    b->out_ids.assign(N, 0);
-    b->out_choice.assign(N, 0);
     b->out_summary.assign(N, 0);
+    b->pool_base.assign(N, 0);
     b->cap_points.assign(N, 0);
-    b->cap_ids.assign(N, 0);
+    b->pool_ids.clear();
+    b->pool_choice.clear();
     b->cls_tab.assign(N, {});
     b->tables.clear();
     b->stats = pb_run_stats{};
     for (int d = 0; d < n_devices; ++d) {
       const pb_batch& s = subs[d];
       const size_t base = out.size();
+      const long long pbase = static_cast<long long>(b->pool_ids.size());
       out.insert(out.end(), s.out.begin(), s.out.end());
+      b->pool_ids.insert(b->pool_ids.end(), s.pool_ids.begin(), s.pool_ids.end());
+      b->pool_choice.insert(b->pool_choice.end(), s.pool_choice.begin(), s.pool_choice.end());
       const int64_t tbase = static_cast<int64_t>(b->tables.size());
       b->tables.insert(b->tables.end(), s.tables.begin(), s.tables.end());
       for (size_t q = 0; q < part[d].size(); ++q) {
         const size_t k = part[d][q];
         b->out_points[k] = base + s.out_points[q];
-        b->out_ids[k] = base + s.out_ids[q];
-        b->out_choice[k] = base + s.out_choice[q];
         b->out_summary[k] = base + s.out_summary[q];
+        b->pool_base[k] = pbase + s.pool_base[q];
         b->cap_points[k] = s.cap_points[q];
-        b->cap_ids[k] = s.cap_ids[q];
         b->cls_tab[k] = s.cls_tab[q];
         for (auto& t : b->cls_tab[k]) t += tbase;
       }
@@ -863,6 +890,12 @@ pb_status pb_batch_points(const pb_batch* b, int32_t k, pb_point* out, int32_t c
   const int32_t np = s.steps + 1;
   if (capacity < np) return fail(PB_ERR_INVALID_ARGUMENT, "points buffer too small");
   std::memcpy(out, b->out.data() + b->out_points[k], sizeof(pb_point) * np);
+  // id_begin: pool offsets on the device -> offsets into pb_batch_deltas()
+  int32_t acc = 0;
+  for (int32_t q = 1; q < np; ++q) {
+    out[q].id_begin = acc;
+    acc += out[q].n_sped + out[q].n_slowed;
+  }
   return PB_OK;
 }
 
@@ -872,8 +905,16 @@ pb_status pb_batch_deltas(const pb_batch* b, int32_t k, int32_t* ids, uint8_t* c
   pb_status st = pb_batch_summary(b, k, &s);
   if (st != PB_OK) return st;
   if (capacity < s.n_ids) return fail(PB_ERR_INVALID_ARGUMENT, "delta buffer too small");
-  if (ids) std::memcpy(ids, b->out.data() + b->out_ids[k], sizeof(int32_t) * s.n_ids);
-  if (choice) std::memcpy(choice, b->out.data() + b->out_choice[k], s.n_ids);
+  const pb_point* pts = reinterpret_cast<const pb_point*>(b->out.data() + b->out_points[k]);
+  int32_t j = 0;
+  for (int32_t q = 1; q <= s.steps; ++q) {
+    const long long at = b->pool_base[k] + pts[q].id_begin;
+    const int32_t cnt = pts[q].n_sped + pts[q].n_slowed;
+    for (int32_t r = 0; r < cnt; ++r, ++j) {
+      if (ids) ids[j] = b->pool_ids[at + r];
+      if (choice) choice[j] = b->pool_choice[at + r];
+    }
+  }
   return PB_OK;
 }
 
@@ -900,8 +941,8 @@ pb_status pb_batch_schedule(const pb_batch* b, int32_t k, int32_t which, int64_t
     ch[i] = choose(c, pt[i]);
   }
   const pb_point* pts = reinterpret_cast<const pb_point*>(b->out.data() + b->out_points[k]);
-  const int32_t* ids = reinterpret_cast<const int32_t*>(b->out.data() + b->out_ids[k]);
-  const uint8_t* cho = reinterpret_cast<const uint8_t*>(b->out.data() + b->out_choice[k]);
+  const int32_t* ids = b->pool_ids.data() + b->pool_base[k];
+  const uint8_t* cho = b->pool_choice.data() + b->pool_base[k];
   for (int32_t q = 1; q <= which; ++q) {
     const pb_point& p = pts[q];
     const int32_t cnt = p.n_sped + p.n_slowed;
@@ -940,6 +981,12 @@ pb_status pb_batch_schedule(const pb_batch* b, int32_t k, int32_t which, int64_t
   }
   if (eff_planned) *eff_planned = effp;
   if (eff_realized) *eff_realized = effr;
+  return PB_OK;
+}
+
+pb_status pb_batch_profile(const pb_batch* b, int64_t* out, int32_t n) {
+  if (!b || !out) return fail(PB_ERR_INVALID_ARGUMENT, "null argument");
+  for (int32_t q = 0; q < n && q < pb::kPrSlots; ++q) out[q] = b->prof[q];
   return PB_OK;
 }
 

@@ -53,11 +53,18 @@ struct DevInst {
   const double* tables;           // E(t) = a exp(b t) + c for t in [t_min, t_max]
   const double* cls_curve;        // [3 * classes] a, b, c (extrapolation only)
   const int64_t* start_planned_t; // get-next mode only
-  // outputs
+  // outputs; delta records go to the batch-wide pool (DeltaPool)
   pb_point* points;             // [cap_points]
-  int32_t* ids;                 // [cap_ids]
-  uint8_t* choice;              // [cap_ids]
   pb_frontier_summary* summary; // [1]
+};
+
+// Batch-wide append-only delta log: each step reserves a contiguous range
+// with one atomicAdd, so only the used prefix is copied back.
+struct DeltaPool {
+  int32_t* ids;      // +(c + 1) sped up, -(c + 1) slowed down
+  uint8_t* choice;   // new Pareto index of that computation
+  unsigned long long* cursor;
+  long long cap;
 };
 
 // Per-CTA workspace slot; arrays sized for the largest instance of a batch.
@@ -66,8 +73,15 @@ struct WsLayout {
   int64_t off_excess, off_tres, off_height, off_mark, off_nr, off_side;
   int64_t off_lower, off_cap, off_flow, off_einf, off_ecrit;
   int64_t off_planned, off_estart, off_lend, off_rstart, off_rdur, off_pdur, off_choice;
-  int64_t off_list0, off_list1, off_bfs0, off_bfs1, off_dead, off_dem, off_delta;
+  int64_t off_list0, off_list1, off_bfs0, off_bfs1, off_dead, off_dem, off_delta, off_tgt;
   int64_t stride;
+};
+
+// Profile slots (pb_batch_profile): cycles per phase (CTA thread 0) and counts.
+enum : int {
+  kPrLp = 0, kPrCap, kPrPhaseA, kPrPhaseB, kPrGr, kPrCut, kPrUpdate, kPrWalk,
+  kPrGrCalls, kPrGrLevels, kPrCutLevels, kPrRoundsA, kPrRoundsB, kPrSteps, kPrMaxRounds, kPrLpLevels,
+  kPrSlots
 };
 
 struct RunCounters {
@@ -75,6 +89,7 @@ struct RunCounters {
   unsigned long long node_updates;
   unsigned long long rounds;
   unsigned long long comp_visits;
+  unsigned long long prof[kPrSlots];
 };
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -115,6 +130,7 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   L.off_dead = take(4 * max_v);
   L.off_dem = take(4 * max_n);
   L.off_delta = take(4 * max_n);
+  L.off_tgt = take(4 * (2 * max_e + max_v));
   L.stride = o;
   return L;
 }
@@ -141,9 +157,10 @@ struct DevFlowJob {
 };
 
 // Host-side launchers (pb_kernels.cu).
+// slots = number of walker warps (one workspace each).
 int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
                  char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
-                 void* stream);
+                 DeltaPool pool, void* stream);
 int walk_slots_per_sm();
 int launch_flow_jobs(const DevFlowJob* d_jobs, int32_t count, char* d_ws, const WsLayout& ws,
                      int32_t slots, void* stream);

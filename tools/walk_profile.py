@@ -1,0 +1,48 @@
+"""Per-phase device profile of the frontier-walk kernel (pb_batch_profile).
+
+  python tools/walk_profile.py config2 [config4 ...] [batch:N]
+"""
+import ctypes as C
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2312_06902_b200 as pb  # noqa: E402
+from paper_2312_06902_b200 import _native as N, g9  # noqa: E402
+
+NAMES = ["lp", "cap", "phaseA", "phaseB", "gr", "cut", "update", "walk", "gr_calls", "gr_levels",
+         "cut_levels", "rounds_A", "rounds_B", "steps", "max_rounds", "lp_levels"]
+
+
+def profile(name):
+    b = pb.FrontierBatch()
+    if name.startswith("config"):
+        b.add_g9(g9.named_config(int(name[-1])))
+    elif name.startswith("batch:"):
+        for i in range(int(name.split(":")[1])):
+            b.add_g9(g9.batch_params(i))
+    t = time.time()
+    b.prepare(0)
+    ms = b.launch()
+    b.fetch()
+    prof = np.zeros(16, np.int64)
+    N.check(N.lib.pb_batch_profile(b._h, N.ptr(prof, C.c_int64), 16))
+    st = b.stats()
+    steps = sum(b.summary(k).steps for k in range(len(b)))
+    bad = [(k, b.summary(k).status, b.summary(k).pad, b.summary(k).steps) for k in range(len(b)) if b.summary(k).status]
+    walk = max(prof[7], 1)
+    print(f"== {name}: kernel {ms:.1f} ms, {steps} steps, {ms * 1e3 / max(steps, 1):.1f} us/step, wall {time.time() - t:.1f}s")
+    print("   cycles share: " + ", ".join(f"{NAMES[i]} {prof[i] / walk:.1%}" for i in range(7)))
+    S = max(prof[13], 1)
+    print("   per step: " + ", ".join(f"{NAMES[i]} {prof[i] / S:.1f}" for i in range(8, 16) if i != 14)
+          + f", max_rounds(one call) {prof[14]}")
+    print(f"   arc_scans/step {st.arc_scans / S:.0f}, node_updates/step {st.node_updates / S:.0f}")
+    if bad:
+        print("   FAILED (index, status, detail, steps):", bad[:10])
+
+
+for name in sys.argv[1:]:
+    profile(name)
