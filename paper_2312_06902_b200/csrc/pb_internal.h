@@ -67,21 +67,23 @@ struct DeltaPool {
   long long cap;
 };
 
-// Per-CTA workspace slot; arrays sized for the largest instance of a batch.
-struct WsLayout {
-  int64_t max_n, max_v, max_e;
-  int64_t off_excess, off_tres, off_height, off_mark, off_nr, off_side;
-  int64_t off_lower, off_cap, off_flow, off_einf, off_ecrit;
-  int64_t off_planned, off_estart, off_lend, off_rstart, off_rdur, off_pdur, off_choice;
-  int64_t off_list0, off_list1, off_bfs0, off_bfs1, off_dead, off_dem, off_delta, off_tgt;
-  int64_t stride;
+// Profile slots (pb_batch_profile): cycles per phase (warp lane 0, summed over
+// warps) and counts.
+enum : int {
+  kPrLp = 0, kPrCap, kPrPhaseA, kPrPhaseB, kPrBfs, kPrAugment, kPrUpdate, kPrWalk,
+  kPrBfsA, kPrBfsB, kPrBfsLevels, kPrPaths, kPrPathHops, kPrSteps, kPrImbalanced, kPrLpLevels,
+  kPrSlots
 };
 
-// Profile slots (pb_batch_profile): cycles per phase (CTA thread 0) and counts.
-enum : int {
-  kPrLp = 0, kPrCap, kPrPhaseA, kPrPhaseB, kPrGr, kPrCut, kPrUpdate, kPrWalk,
-  kPrGrCalls, kPrGrLevels, kPrCutLevels, kPrRoundsA, kPrRoundsB, kPrSteps, kPrMaxRounds, kPrLpLevels,
-  kPrSlots
+// Per-warp workspace slot; arrays sized for the largest instance of a batch.
+// The flow f[] persists across the steps of a walk (warm start).
+struct WsLayout {
+  int64_t max_n, max_v, max_e;
+  int64_t off_lo, off_up, off_f, off_inf, off_crit;      // per edge
+  int64_t off_bal, off_vis, off_par, off_mk;             // per node
+  int64_t off_planned, off_estart, off_lend, off_rstart, off_rdur, off_pdur, off_choice;  // per comp
+  int64_t off_f0, off_f1, off_touch, off_exl, off_delta;  // lists
+  int64_t stride;
 };
 
 struct RunCounters {
@@ -105,17 +107,15 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
     o = align_up(o + bytes, 256);
     return at;
   };
-  L.off_excess = take(8 * max_v);
-  L.off_tres = take(8 * max_v);
-  L.off_height = take(4 * max_v);
-  L.off_mark = take(4 * max_v);
-  L.off_nr = take(max_v);
-  L.off_side = take(4 * max_v);
-  L.off_lower = take(8 * max_e);
-  L.off_cap = take(8 * max_e);
-  L.off_flow = take(8 * max_e);
-  L.off_einf = take(max_e);
-  L.off_ecrit = take(max_e);
+  L.off_lo = take(8 * max_e);
+  L.off_up = take(8 * max_e);
+  L.off_f = take(8 * max_e);
+  L.off_inf = take(max_e);
+  L.off_crit = take(max_e);
+  L.off_bal = take(8 * max_v);
+  L.off_vis = take(4 * max_v);
+  L.off_par = take(4 * max_v);
+  L.off_mk = take(4 * max_v);
   L.off_planned = take(8 * max_n);
   L.off_estart = take(8 * max_n);
   L.off_lend = take(8 * max_n);
@@ -123,14 +123,11 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   L.off_rdur = take(8 * max_n);
   L.off_pdur = take(8 * max_n);
   L.off_choice = take(max_n);
-  L.off_list0 = take(4 * max_v);
-  L.off_list1 = take(4 * max_v);
-  L.off_bfs0 = take(4 * max_v);
-  L.off_bfs1 = take(4 * max_v);
-  L.off_dead = take(4 * max_v);
-  L.off_dem = take(4 * max_n);
+  L.off_f0 = take(4 * max_v);
+  L.off_f1 = take(4 * max_v);
+  L.off_touch = take(4 * 2 * max_e);
+  L.off_exl = take(4 * max_v);
   L.off_delta = take(4 * max_n);
-  L.off_tgt = take(4 * (2 * max_e + max_v));
   L.stride = o;
   return L;
 }

@@ -3,11 +3,8 @@
 // One WARP walks one instance's whole frontier (frontier.hpp:166-189) inside
 // a single persistent launch: warps pull instances (LPT order) from a global
 // counter, so thousands of walks are in flight and no host round trip
-// happens per step.  The graphs are deep and narrow (<= ~2N nodes per level,
-// SURVEY.md §7 hard part 7), so a warp covers a level; all synchronization
-// is __syncwarp, all appends are ballot compactions, and deduplication is
-// __match_any_sync + a round stamp (no global atomics with return values on
-// the critical path).  Per step:
+// happens per step.  All synchronization is __syncwarp, appends are ballot
+// compactions, deduplication is __match_any_sync + a stamp.  Per step:
 //
 //   K2  longest path over static node-DAG levels (annotate_slack,
 //       dag.hpp:233-286; simulate, emulator.hpp:28-55): pull-based,
@@ -15,18 +12,24 @@
 //   K3  fused critical mask + Eq. 7 capacities (build_capacity_dag,
 //       flow.hpp:285-317) from host-tabulated curve values, with the
 //       reference's int128 overflow checks (flow.hpp:58-68, 196-197);
-//   K4  push-relabel max flow with lower bounds: phase A = feasibility
-//       circulation with netted demands (flow.hpp:172-203), phase B =
-//       source->sink max preflow on the same residual arrays
-//       (flow.hpp:205-228), global relabel by backward BFS;
-//   K5  minimal min cut = residual reachability from {s} U {excess nodes}
-//       (min_cut_from_flow's source side, flow.hpp:234-278), tau update with
-//       the reference's skip rules (frontier.hpp:111-131), discretize
-//       (frontier.hpp:140-161), realized longest path, append-only delta log.
+//   K4  max flow with lower bounds, WARM-STARTED: the flow of the previous
+//       step is kept, clamped into the new bounds (edges leaving the critical
+//       sub-DAG drop to 0, new ones start at their lower bound), and the
+//       resulting node imbalances are repaired by multi-source BFS
+//       augmentation in the circulation network with the return arc
+//       sink->source (phase A = the feasibility test of flow.hpp:172-203);
+//       phase B then augments source->sink along BFS-shortest residual
+//       paths (flow.hpp:205-228).  Steps change few capacities, so a step
+//       needs ~1-4 BFS instead of a from-scratch max flow;
+//   K5  the last phase-B BFS (sink unreachable) visits exactly the source
+//       side of the minimal minimum cut (min_cut_from_flow, flow.hpp:234-262);
+//       tau update with the reference's skip rules (frontier.hpp:111-131),
+//       discretize (frontier.hpp:140-161), realized longest path,
+//       append-only delta log.
 //
 // Only the unique minimal min cut and the two verdicts (feasible, value >=
-// sentinel) feed the outputs, so the flow algorithm is free to differ from
-// the reference's Edmonds-Karp (SURVEY.md §7 parity rule 1).
+// sentinel) feed the outputs, so the flow itself is free to differ from the
+// reference's Edmonds-Karp flow (SURVEY.md §7 parity rule 1).
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -40,6 +43,7 @@ namespace {
 constexpr int kWarpsPerBlock = 4;
 constexpr int kBlock = 32 * kWarpsPerBlock;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr long long kHuge = LLONG_MAX / 4;  // return-arc capacity (never binding)
 typedef __int128 i128;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -83,7 +87,6 @@ __device__ __forceinline__ void wappend(bool pred, int val, int32_t* list, int& 
   count += __popc(m);
 }
 
-__device__ __forceinline__ long long ldcg(const int64_t* p) { return __ldcg(p); }
 __device__ __forceinline__ void red_add(int64_t* p, long long d) {
   atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(d));
 }
@@ -94,323 +97,73 @@ struct Counters {
   __device__ void add(int slot, long long v) {
     if (lane_id() == 0) prof[slot] += static_cast<unsigned long long>(v);
   }
-  __device__ void maxv(int slot, long long v) {
-    if (lane_id() == 0 && static_cast<unsigned long long>(v) > prof[slot]) prof[slot] = v;
-  }
 };
 
 __device__ __forceinline__ long long now() { return clock64(); }
 
-// Flow-network view of one warp's workspace.
+// Flow-network view of one warp's workspace.  Edge ids: graph edges, then the
+// return arc `ret` (sink -> source, capacity kHuge, enabled in phase A only);
+// f[ret] is the circulation's s->t value R.
 struct Net {
-  int V, E, src, snk, ret;  // E counts graph edges + the return arc (index ret)
+  int V, E, src, snk, ret;
   const int32_t* inc_off;
   const int32_t* inc;  // (edge << 1) | dir, dir = 1 when the node is the head
   const int32_t* tail;
   const int32_t* head;
-  int64_t* lower;
-  int64_t* cap;   // resolved upper - lower (0 for absent edges)
-  int64_t* flow;  // f - lower
-  uint8_t* einf;
-  uint8_t* ecrit;
-  int64_t* excess;
-  int64_t* tres;  // phase-A residual to the super sink t'
-  int32_t* height;
-  int32_t* mark;
-  uint8_t* nr;
-  int32_t* side;
-  int32_t* list0;
-  int32_t* list1;
-  int32_t* bfs0;
-  int32_t* bfs1;
-  int32_t* dead;
-  int32_t* dem;  // nodes with a super-sink arc (phase A)
-  int32_t* tgt;  // push targets of one round (with duplicates)
-  // warp-uniform bookkeeping
-  int n_dead, n_dem, stamp, flag;
+  int64_t* lo;
+  int64_t* up;  // finite upper bound (ignored when inf)
+  int64_t* f;   // absolute flow, persistent across steps
+  uint8_t* inf;
+  uint8_t* crit;  // edge present in the current network
+  int64_t* bal;   // inflow - outflow (phase-A imbalance)
+  int32_t* vis;   // BFS stamp
+  int32_t* par;   // BFS parent code (edge << 1) | backward
+  int32_t* mk;    // list dedup stamp
+  int32_t* f0;
+  int32_t* f1;
+  int32_t* touch;
+  int32_t* exl;
+  long long sentinel;
+  int stamp, mstamp;
+  bool ret_on;
 };
 
-__device__ __forceinline__ long long residual_out(const Net& N, int a) {
+__device__ __forceinline__ long long upres(const Net& N, int ed) {
+  return ed == N.ret ? kHuge : (N.inf[ed] ? N.sentinel : N.up[ed]);
+}
+// Residual capacity of traversing incidence entry a away from its node:
+// forward (node is tail) = upper - f, backward (node is head) = f - lower.
+__device__ __forceinline__ long long residual_from(const Net& N, int a) {
   const int ed = a >> 1;
-  return (a & 1) ? N.flow[ed] : N.cap[ed] - N.flow[ed];
+  if (ed == N.ret ? !N.ret_on : !N.crit[ed]) return 0;
+  return (a & 1) ? N.f[ed] - N.lo[ed] : upres(N, ed) - N.f[ed];
 }
 __device__ __forceinline__ int other_end(const Net& N, int a) {
   const int ed = a >> 1;
   return (a & 1) ? N.tail[ed] : N.head[ed];
 }
 
-// Global relabel: exact residual distances to the sink (phase B) or to the
-// super sink t' (phase A; distance 1 for nodes with tres > 0).  Unreached
-// nodes get H.  Heights only grow, so labels stay valid.
-__device__ void global_relabel(Net& N, bool phaseA, int H, Counters& C) {
+// Level-synchronous BFS over residual arcs from `nsrc` sources in N.f0.
+// phaseA: targets are nodes with bal < 0; phaseB: the sink.  Stops at the
+// first level that reaches a target and returns it (-1: none reachable; then
+// the stamp N.stamp marks exactly the residual-reachable set).
+__device__ int bfs(Net& N, int nsrc, bool phaseA, Counters& C) {
   const int ln = lane_id();
   const long long t0 = now();
-  C.add(kPrGrCalls, 1);
-  for (int v = ln; v < N.V; v += 32) N.height[v] = H;
-  __syncwarp();
-  int cnt = 0;
-  if (phaseA) {
-    for (int base = 0; base < N.n_dem; base += 32) {
-      const int i = base + ln;
-      const int v = i < N.n_dem ? N.dem[i] : 0;
-      const bool ok = i < N.n_dem && N.tres[v] > 0;
-      if (ok) N.height[v] = 1;
-      wappend(ok, v, N.bfs0, cnt);
-    }
-  } else {
-    if (ln == 0) {
-      N.height[N.snk] = 0;
-      N.bfs0[0] = N.snk;
-    }
-    cnt = 1;
-  }
-  __syncwarp();
-  int32_t* F = N.bfs0;
-  int32_t* G = N.bfs1;
-  int level = phaseA ? 1 : 0;
-  while (cnt > 0) {
-    C.add(kPrGrLevels, 1);
-    int nc = 0;
-    for (int base = 0; base < cnt; base += 32) {
-      const int i = base + ln;
-      const bool valid = i < cnt;
-      const int w = valid ? F[i] : 0;
-      const int off = valid ? N.inc_off[w] : 0;
-      const int deg = valid ? N.inc_off[w + 1] - off : 0;
-      const int md = wmaxi(deg);
-      if (valid) C.arc_scans += deg;
-      for (int j = 0; j < md; ++j) {
-        bool cand = false;
-        int u = 0;
-        if (j < deg) {
-          const int a = N.inc[off + j];
-          const int ed = a >> 1;
-          u = (a & 1) ? N.tail[ed] : N.head[ed];
-          // arc u -> w: forward of ed when w is the head, backward otherwise
-          const long long r = (a & 1) ? N.cap[ed] - N.flow[ed] : N.flow[ed];
-          cand = r > 0 && N.height[u] == H && (phaseA || u != N.src);
-        }
-        // one writer per distinct u among the lanes of this instruction
-        const unsigned peers = __match_any_sync(kFull, cand ? u : -1 - ln);
-        const bool lead = cand && (__ffs(peers) - 1) == ln;
-        if (lead) N.height[u] = level + 1;
-        wappend(lead, u, G, nc);
-        __syncwarp();
-      }
-    }
-    __syncwarp();
-    cnt = nc;
-    ++level;
-    int32_t* t = F;
-    F = G;
-    G = t;
-  }
-  C.add(kPrGr, now() - t0);
-}
-
-// Keeps list entries with excess and height < H.  Phase A: excess stranded
-// at H means the circulation is infeasible (N.flag).  Phase B: stranded
-// excess goes to the dead list (it seeds the cut BFS).
-__device__ int filter_active(Net& N, bool phaseA, int H, const int32_t* from, int cnt, int32_t* to) {
-  const int ln = lane_id();
-  int out = 0;
-  for (int base = 0; base < cnt; base += 32) {
-    const int i = base + ln;
-    const int v = i < cnt ? from[i] : 0;
-    const bool has = i < cnt && ldcg(&N.excess[v]) > 0;
-    const bool live = has && N.height[v] < H;
-    const bool stuck = has && !live;
-    if (phaseA) {
-      if (__any_sync(kFull, stuck)) N.flag = 1;
-    } else {
-      wappend(stuck, v, N.dead, N.n_dead);
-    }
-    wappend(live, v, to, out);
-  }
-  __syncwarp();
-  return out;
-}
-
-// Dedups the round's push targets (+ nodes keeping excess) into the next
-// worklist: __match_any_sync elects one lane per node within a chunk, the
-// round stamp filters repeats across chunks.
-__device__ int build_next(Net& N, int ntgt, int32_t* nxt) {
-  const int ln = lane_id();
   ++N.stamp;
   const int stamp = N.stamp;
-  int cnt = 0;
-  for (int base = 0; base < ntgt; base += 32) {
-    const int i = base + ln;
-    const bool valid = i < ntgt;
-    const int w = valid ? N.tgt[i] : 0;
-    const unsigned peers = __match_any_sync(kFull, valid ? w : -1 - ln);
-    bool fresh = valid && (__ffs(peers) - 1) == ln && N.mark[w] != stamp;
-    if (fresh) N.mark[w] = stamp;
-    wappend(fresh, w, nxt, cnt);
-    __syncwarp();
+  for (int i = ln; i < nsrc; i += 32) {
+    const int v = N.f0[i];
+    N.vis[v] = stamp;
+    N.par[v] = -1;
   }
-  return cnt;
-}
-
-// Synchronous push-relabel rounds.  Push sub-phase: every active node pushes
-// along admissible arcs (h(v) == h(w) + 1) against a fixed height snapshot,
-// so each arc has one writer per sub-phase; excess arrives by integer REDs
-// (order-independent).  Relabel sub-phase: nodes left with excess take
-// 1 + min residual-neighbour height (valid under concurrent relabels because
-// heights only increase).  Returns 0 when no active node is left, 1 if
-// phase A proves infeasibility, 2 if the round watchdog fires (a bug guard
-// that turns a would-be hang into a PB_ERR_LOGIC status).
-__device__ int push_relabel(Net& N, bool phaseA, int H, int cnt, Counters& C) {
-  const int ln = lane_id();
-  int32_t* cur = N.list0;
-  int32_t* nxt = N.list1;
-  long long relabels_since = 0;
-  const long long gr_threshold = N.V > 64 ? N.V : 64;
-  const long long max_rounds = 64ll * N.V + 100000;
-  long long rounds = 0;
-  while (cnt > 0) {
-    C.add(phaseA ? kPrRoundsA : kPrRoundsB, 1);
-    ++C.rounds;
-    if (++rounds > max_rounds) return 2;
-    C.maxv(kPrMaxRounds, rounds);
-    // ---- push
-    int ntgt = 0;
-    for (int base = 0; base < cnt; base += 32) {
-      const int i = base + ln;
-      const bool valid = i < cnt;
-      const int v = valid ? cur[i] : 0;
-      const int hv = valid ? N.height[v] : H;
-      long long e = valid ? ldcg(&N.excess[v]) : 0;
-      const bool act = valid && e > 0 && hv < H;
-      long long pushed = 0;
-      if (phaseA && act && hv == 1) {
-        const long long tr = N.tres[v];
-        if (tr > 0) {
-          const long long d = e < tr ? e : tr;
-          N.tres[v] = tr - d;
-          e -= d;
-          pushed += d;
-          ++C.node_updates;
-        }
-      }
-      const int off = act ? N.inc_off[v] : 0;
-      const int deg = act ? N.inc_off[v + 1] - off : 0;
-      const int md = wmaxi(deg);
-      for (int j = 0; j < md; ++j) {
-        bool push = false;
-        int w = 0;
-        if (j < deg && e > 0) {
-          const int a = N.inc[off + j];
-          ++C.arc_scans;
-          w = other_end(N, a);
-          if (N.height[w] == hv - 1) {
-            const long long r = residual_out(N, a);
-            if (r > 0) {
-              const long long d = e < r ? e : r;
-              N.flow[a >> 1] += (a & 1) ? -d : d;
-              e -= d;
-              pushed += d;
-              red_add(&N.excess[w], d);
-              ++C.node_updates;
-              push = phaseA || (w != N.snk && w != N.src);
-            }
-          }
-        }
-        wappend(push, w, N.tgt, ntgt);
-      }
-      if (pushed) red_add(&N.excess[v], -pushed);
-      if (act && e > 0) N.nr[v] = 1;
-    }
-    __syncwarp();
-    // ---- relabel
-    int relabeled = 0;
-    bool stuck_any = false;
-    for (int base = 0; base < cnt; base += 32) {
-      const int i = base + ln;
-      const bool valid = i < cnt;
-      const int v = valid ? cur[i] : 0;
-      const bool rl = valid && N.nr[v];
-      const int off = rl ? N.inc_off[v] : 0;
-      const int deg = rl ? N.inc_off[v + 1] - off : 0;
-      const int md = wmaxi(deg);
-      int mh = INT_MAX;
-      if (rl && phaseA && N.tres[v] > 0) mh = 0;
-      for (int j = 0; j < md; ++j) {
-        if (j < deg) {
-          const int a = N.inc[off + j];
-          if (residual_out(N, a) > 0) {
-            const int hw = N.height[other_end(N, a)];
-            mh = hw < mh ? hw : mh;
-          }
-        }
-      }
-      if (rl) {
-        C.arc_scans += deg;
-        N.nr[v] = 0;
-        N.height[v] = (mh == INT_MAX || mh + 1 >= H) ? H : mh + 1;
-        ++C.node_updates;
-      }
-      relabeled += __popc(__ballot_sync(kFull, rl));
-      __syncwarp();
-      const bool has = valid && ldcg(&N.excess[v]) > 0;
-      const bool live = has && N.height[v] < H;
-      const bool stuck = has && !live;
-      wappend(live, v, N.tgt, ntgt);
-      if (phaseA) {
-        stuck_any |= __any_sync(kFull, stuck);
-      } else {
-        wappend(stuck, v, N.dead, N.n_dead);
-      }
-    }
-    __syncwarp();
-    if (stuck_any) return 1;
-    cnt = build_next(N, ntgt, nxt);
-    relabels_since += relabeled;
-    int32_t* t = cur;
-    cur = nxt;
-    nxt = t;
-    if (cnt > 0 && relabels_since >= gr_threshold) {
-      relabels_since = 0;
-      global_relabel(N, phaseA, H, C);
-      N.flag = 0;
-      cnt = filter_active(N, phaseA, H, cur, cnt, nxt);
-      if (phaseA && N.flag) return 1;
-      t = cur;
-      cur = nxt;
-      nxt = t;
-    }
-  }
-  return 0;
-}
-
-// Reachability from {source} U dead-list (excess) nodes over residual arcs:
-// the source side of the minimal minimum cut (flow.hpp:234-262).
-__device__ void cut_bfs(Net& N, Counters& C) {
-  const int ln = lane_id();
-  const long long t0 = now();
-  for (int v = ln; v < N.V; v += 32) N.side[v] = 0;
   __syncwarp();
-  int cnt = 0;
-  if (ln == 0) {
-    N.side[N.src] = 1;
-    N.bfs0[0] = N.src;
-  }
-  cnt = 1;
-  __syncwarp();
-  for (int base = 0; base < N.n_dead; base += 32) {
-    const int i = base + ln;
-    const int v = i < N.n_dead ? N.dead[i] : 0;
-    bool ok = i < N.n_dead && v != N.snk && v != N.src && ldcg(&N.excess[v]) > 0;
-    const unsigned peers = __match_any_sync(kFull, ok ? v : -1 - ln);
-    ok = ok && (__ffs(peers) - 1) == ln && N.side[v] == 0;
-    if (ok) N.side[v] = 1;
-    wappend(ok, v, N.bfs0, cnt);
-    __syncwarp();
-  }
-  int32_t* F = N.bfs0;
-  int32_t* G = N.bfs1;
-  while (cnt > 0) {
-    C.add(kPrCutLevels, 1);
+  int cnt = nsrc;
+  int32_t* F = N.f0;
+  int32_t* G = N.f1;
+  int found = -1;
+  while (cnt > 0 && found < 0) {
+    C.add(kPrBfsLevels, 1);
     int nc = 0;
     for (int base = 0; base < cnt; base += 32) {
       const int i = base + ln;
@@ -422,17 +175,25 @@ __device__ void cut_bfs(Net& N, Counters& C) {
       if (valid) C.arc_scans += deg;
       for (int j = 0; j < md; ++j) {
         bool cand = false;
-        int u = 0;
+        int u = 0, a = 0;
         if (j < deg) {
-          const int a = N.inc[off + j];
-          if (residual_out(N, a) > 0) {
+          a = N.inc[off + j];
+          if (residual_from(N, a) > 0) {
             u = other_end(N, a);
-            cand = N.side[u] == 0;
+            cand = N.vis[u] != stamp;
           }
         }
         const unsigned peers = __match_any_sync(kFull, cand ? u : -1 - ln);
         const bool lead = cand && (__ffs(peers) - 1) == ln;
-        if (lead) N.side[u] = 1;
+        bool hit = false;
+        if (lead) {
+          N.vis[u] = stamp;
+          N.par[u] = ((a >> 1) << 1) | (a & 1);
+          ++C.node_updates;
+          hit = phaseA ? N.bal[u] < 0 : u == N.snk;
+        }
+        const unsigned h = __ballot_sync(kFull, hit);
+        if (h && found < 0) found = __shfl_sync(kFull, u, __ffs(h) - 1);
         wappend(lead, u, G, nc);
         __syncwarp();
       }
@@ -443,101 +204,118 @@ __device__ void cut_bfs(Net& N, Counters& C) {
     G = t;
   }
   __syncwarp();
-  C.add(kPrCut, now() - t0);
+  C.add(kPrBfs, now() - t0);
+  return found;
 }
 
-// Phase A (feasibility) + phase B (max preflow) + value, on a network whose
-// lower/cap/einf/ecrit/flow(=0) arrays are set, demand list N.dem (nodes with
-// tres > 0) and the initial phase-A worklist in list0 (n_init entries).
-// Excess and tres must be zero elsewhere.  Returns 0 ok, 1 infeasible,
-// 2 watchdog.  *value = net flow into the sink.
-__device__ int solve_flow(Net& N, long long return_cap, int n_init, long long* value, Counters& C,
-                          int* detail) {
+// Augments along the BFS parent chain ending at `tgt` (lane 0; the path is a
+// pointer chase).  Phase A: amount = min(residuals, bal[src], -bal[tgt]) and
+// the balances move; phase B: amount = min(residuals) and R grows.
+__device__ void augment(Net& N, int tgt, bool phaseA, Counters& C) {
+  const long long t0 = now();
+  if (lane_id() == 0) {
+    long long d = phaseA ? -N.bal[tgt] : LLONG_MAX;
+    int v = tgt, hops = 0;
+    while (N.par[v] != -1) {
+      const int code = N.par[v];
+      const int ed = code >> 1;
+      const long long r = (code & 1) ? N.f[ed] - N.lo[ed] : upres(N, ed) - N.f[ed];
+      d = r < d ? r : d;
+      v = (code & 1) ? N.head[ed] : N.tail[ed];
+      ++hops;
+    }
+    if (phaseA) d = N.bal[v] < d ? N.bal[v] : d;
+    const int src = v;
+    v = tgt;
+    while (N.par[v] != -1) {
+      const int code = N.par[v];
+      const int ed = code >> 1;
+      N.f[ed] += (code & 1) ? -d : d;
+      v = (code & 1) ? N.head[ed] : N.tail[ed];
+    }
+    if (phaseA) {
+      N.bal[src] -= d;
+      N.bal[tgt] += d;
+    } else {
+      N.f[N.ret] += d;
+    }
+    C.prof[kPrPaths] += 1;
+    C.prof[kPrPathHops] += hops;
+    C.node_updates += 2 * hops;
+  }
+  __syncwarp();
+  C.add(kPrAugment, now() - t0);
+}
+
+// Phase A: repairs the imbalances of the nodes in N.touch (ntouch entries,
+// duplicates allowed) in the circulation network (return arc enabled).
+// Returns false when some excess cannot reach any deficit: the bounded
+// network is infeasible (max_flow_lower_bounds returns nullopt).
+__device__ bool repair(Net& N, int ntouch, Counters& C) {
   const int ln = lane_id();
-  long long t0 = now();
-  if (N.n_dem > 0 || n_init > 0) {
-    if (ln == 0) {
-      N.cap[N.ret] = return_cap;
-      N.flow[N.ret] = 0;
+  // distinct touched nodes with excess
+  ++N.mstamp;
+  int nex = 0;
+  for (int base = 0; base < ntouch; base += 32) {
+    const int i = base + ln;
+    const bool valid = i < ntouch;
+    const int v = valid ? N.touch[i] : 0;
+    const unsigned peers = __match_any_sync(kFull, valid ? v : -1 - ln);
+    bool take = valid && (__ffs(peers) - 1) == ln && N.mk[v] != N.mstamp;
+    if (take) N.mk[v] = N.mstamp;
+    take = take && N.bal[v] > 0;
+    wappend(take, v, N.exl, nex);
+    __syncwarp();
+  }
+  if (nex == 0) return true;
+  C.add(kPrImbalanced, nex);
+  const long long t0 = now();
+  N.ret_on = true;
+  bool ok = true;
+  for (;;) {
+    int ns = 0;
+    for (int base = 0; base < nex; base += 32) {
+      const int i = base + ln;
+      const int v = i < nex ? N.exl[i] : 0;
+      wappend(i < nex && N.bal[v] > 0, v, N.f0, ns);
     }
     __syncwarp();
-    const int HA = N.V + 2;
-    global_relabel(N, true, HA, C);
-    N.flag = 0;
-    int cnt = filter_active(N, true, HA, N.list0, n_init, N.list1);
-    if (N.flag) return 1;
-    for (int i = ln; i < cnt; i += 32) N.list0[i] = N.list1[i];
+    if (ns == 0) break;
+    for (int i = ln; i < ns; i += 32) N.exl[i] = N.f0[i];
+    nex = ns;
     __syncwarp();
-    const int rc = push_relabel(N, true, HA, cnt, C);
-    if (rc == 2) *detail = 1;
-    if (rc) return rc;
+    C.add(kPrBfsA, 1);
+    const int tgt = bfs(N, ns, true, C);
+    if (tgt < 0) {
+      ok = false;
+      break;
+    }
+    augment(N, tgt, true, C);
   }
+  N.ret_on = false;
   C.add(kPrPhaseA, now() - t0);
-  t0 = now();
-  // ---- phase B: drop the return arc, saturate every residual arc out of s
-  if (ln == 0) {
-    N.cap[N.ret] = 0;
-    N.flow[N.ret] = 0;
-  }
-  N.n_dead = 0;
-  __syncwarp();
-  const int HB = N.V;
-  int cnt = 0;
-  {
-    const int off = N.inc_off[N.src], deg = N.inc_off[N.src + 1] - off;
-    for (int base = 0; base < deg; base += 32) {
-      const int j = base + ln;
-      bool ok = false;
-      int w = 0;
-      if (j < deg) {
-        const int a = N.inc[off + j];
-        const long long r = residual_out(N, a);
-        if (r > 0) {
-          w = other_end(N, a);
-          N.flow[a >> 1] += (a & 1) ? -r : r;
-          red_add(&N.excess[w], r);
-          ok = w != N.snk && w != N.src;
-        }
-      }
-      wappend(ok, w, N.tgt, cnt);
-    }
-  }
-  __syncwarp();
-  cnt = build_next(N, cnt, N.list1);
-  global_relabel(N, false, HB, C);
-  if (ln == 0) N.height[N.src] = HB;
-  __syncwarp();
-  cnt = filter_active(N, false, HB, N.list1, cnt, N.list0);
-  if (push_relabel(N, false, HB, cnt, C)) {
-    *detail = 2;
-    return 2;
+  return ok;
+}
+
+// Phase B: source->sink augmentation until the sink is unreachable; the
+// last BFS stamp then marks the minimal min cut's source side.
+__device__ void maximize(Net& N, Counters& C) {
+  const long long t0 = now();
+  for (;;) {
+    if (lane_id() == 0) N.f0[0] = N.src;
+    __syncwarp();
+    C.add(kPrBfsB, 1);
+    const int tgt = bfs(N, 1, false, C);
+    if (tgt < 0) break;
+    augment(N, tgt, false, C);
   }
   C.add(kPrPhaseB, now() - t0);
-  // value = net flow into the sink over graph edges
-  long long vloc = 0;
-  {
-    const int off = N.inc_off[N.snk], deg = N.inc_off[N.snk + 1] - off;
-    for (int j = ln; j < deg; j += 32) {
-      const int a = N.inc[off + j];
-      const int ed = a >> 1;
-      if (ed == N.ret || !N.ecrit[ed]) continue;
-      const long long f = N.lower[ed] + N.flow[ed];
-      vloc += (a & 1) ? f : -f;
-    }
-  }
-  *value = wsum(vloc);
-  return 0;
 }
 
-// Restores excess == 0 everywhere after phase B (dead nodes, sink).
-__device__ void clear_excess(Net& N) {
-  const int ln = lane_id();
-  for (int i = ln; i < N.n_dead; i += 32) N.excess[N.dead[i]] = 0;
-  if (ln == 0) {
-    N.excess[N.snk] = 0;
-    N.excess[N.src] = 0;
-  }
-  __syncwarp();
+// Records a flow change on edge ed: imbalance at both ends, both touched.
+__device__ __forceinline__ void flow_change(Net& N, int ed, long long delta) {
+  red_add(&N.bal[N.head[ed]], delta);
+  red_add(&N.bal[N.tail[ed]], -delta);
 }
 
 // ------------------------------------------------------------------ walk
@@ -661,6 +439,45 @@ __device__ void write_point(const DevInst& I, int k, long long tp, long long tr,
   I.points[k] = p;
 }
 
+__device__ void reset_net(Net& N) {
+  const int ln = lane_id();
+  for (int e = ln; e < N.E; e += 32) {
+    N.f[e] = 0;
+    N.lo[e] = 0;
+    N.up[e] = 0;
+    N.inf[e] = 0;
+    N.crit[e] = 0;
+  }
+  for (int v = ln; v < N.V; v += 32) {
+    N.bal[v] = 0;
+    N.vis[v] = 0;
+    N.mk[v] = 0;
+  }
+  N.stamp = 0;
+  N.mstamp = 0;
+  N.ret_on = false;
+  N.sentinel = 0;
+  __syncwarp();
+}
+
+// Clamps every infinite critical edge's flow to the new sentinel (only
+// needed when the sentinel shrank below a carried flow; checked by caller).
+__device__ void clamp_infinite(Net& N, int nedges, int& ntouch) {
+  const int ln = lane_id();
+  for (int base = 0; base < nedges; base += 32) {
+    const int k = base + ln;
+    bool ch = false;
+    if (k < nedges && N.crit[k] && N.inf[k] && N.f[k] > N.sentinel) {
+      flow_change(N, k, N.sentinel - N.f[k]);
+      N.f[k] = N.sentinel;
+      ch = true;
+    }
+    wappend(ch, ch ? N.tail[k] : 0, N.touch, ntouch);
+    wappend(ch, ch ? N.head[k] : 0, N.touch, ntouch);
+  }
+  __syncwarp();
+}
+
 __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& pool, Counters& C) {
   const int ln = lane_id();
   const int n = I.n;
@@ -673,26 +490,8 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   N.inc = I.inc;
   N.tail = I.ec_tail;
   N.head = I.ec_head;
-  N.stamp = 1;
-  N.n_dead = 0;
-  N.n_dem = 0;
-  N.flag = 0;
+  reset_net(N);
 
-  // ---- reset workspace for this instance
-  for (int v = ln; v < N.V; v += 32) {
-    N.excess[v] = 0;
-    N.tres[v] = 0;
-    N.mark[v] = 0;
-    N.nr[v] = 0;
-    N.height[v] = 0;
-  }
-  for (int e = ln; e < N.E; e += 32) {
-    N.flow[e] = 0;
-    N.cap[e] = 0;
-    N.lower[e] = 0;
-    N.ecrit[e] = 0;
-    N.einf[e] = 0;
-  }
   int bad = 0;
   long long spe = 0, spt = 0, sre = 0, srt = 0;
   for (int i = ln; i < n; i += 32) {
@@ -729,6 +528,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   long long n_ids = 0;
   int status = PB_OK;
   int stop = PB_STOP_AT_TMIN;
+  const int nedges = n + I.ne;
 
   for (;;) {
     long long step;
@@ -751,23 +551,21 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     }
     // ---- K2 backward pass (latest) on the current planned durations
     backward_pass(I, W.planned, W.lend, t_cur, C);
-    // ---- K3 critical mask + capacities
+    // ---- K3 critical mask + capacities; carried flow clamped into the new bounds
     const long long tcap = now();
     C.add(kPrSteps, 1);
     i128 suml = 0, sumu = 0;
-    long long ninf = 0;
-    int n_init = 0;
-    N.n_dem = 0;
+    long long ninf = 0, max_inf_f = 0;
+    int ntouch = 0;
     for (int base = 0; base < n; base += 32) {
       const int i = base + ln;
-      const bool valid = i < n;
-      long long l = 0, capv = 0;
-      uint8_t inf = 1;
-      bool crit = false;
-      if (valid) {
+      bool ch = false;
+      if (i < n) {
         const int c = I.comp_class[i];
         const long long t = W.planned[i];
-        crit = W.estart[i] + t == W.lend[i];
+        const bool crit = W.estart[i] + t == W.lend[i];
+        long long l = 0, u = 0;
+        uint8_t inf = 1;
         if (crit && !I.cls_const[c]) {
           const long long tmin = I.cls_tmin[c], tmax = I.cls_tmax[c];
           const bool can_speed = t - step >= tmin;
@@ -779,122 +577,119 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
           }
           if (can_speed) {
             const long long r = llround(table_at(I, c, t - step, &bad) - et);
-            capv = (r > l ? r : l) - l;
+            u = r > l ? r : l;
             inf = 0;
           }
         }
-        N.ecrit[i] = crit;
-        N.lower[i] = crit ? l : 0;
-        N.einf[i] = inf;
-        N.cap[i] = crit ? capv : 0;
-        N.flow[i] = 0;
+        const long long fo = N.f[i];
+        long long fn = 0;
         if (crit) {
+          fn = fo < l ? l : fo;
+          if (!inf && fn > u) fn = u;
           suml += l;
           if (!inf)
-            sumu += l + capv;
-          else
+            sumu += u;
+          else {
             ++ninf;
+            max_inf_f = fn > max_inf_f ? fn : max_inf_f;
+          }
         }
-        if (crit && l > 0) {
-          N.tres[2 * i] = l;
-          N.excess[2 * i + 1] = l;
+        N.lo[i] = l;
+        N.up[i] = u;
+        N.inf[i] = inf;
+        N.crit[i] = crit;
+        if (fn != fo) {
+          N.f[i] = fn;
+          flow_change(N, i, fn - fo);
+          ch = true;
         }
       }
-      const bool dem = valid && crit && l > 0;
-      wappend(dem, 2 * i, N.dem, N.n_dem);
-      wappend(dem, 2 * i + 1, N.list0, n_init);
+      wappend(ch, 2 * i, N.touch, ntouch);
+      wappend(ch, 2 * i + 1, N.touch, ntouch);
     }
-    for (int j = ln; j < I.ne; j += 32) {
-      const int u = I.dep_tail[j], v = I.dep_head[j];
+    for (int base = 0; base < I.ne; base += 32) {
+      const int j = base + ln;
+      bool ch = false;
       const int k = n + j;
-      long long te, he;
-      bool tc, hc;
-      if (u == n) {
-        te = 0;
-        tc = true;  // latest[source] == 0 whenever a critical head exists
-      } else {
-        te = W.estart[u] + W.planned[u];
-        tc = te == W.lend[u];
+      if (j < I.ne) {
+        const int u = I.dep_tail[j], v = I.dep_head[j];
+        long long te, he;
+        bool tc, hc;
+        if (u == n) {
+          te = 0;
+          tc = true;  // latest[source] == 0 whenever a critical head exists
+        } else {
+          te = W.estart[u] + W.planned[u];
+          tc = te == W.lend[u];
+        }
+        if (v == n + 1) {
+          he = t_cur;
+          hc = true;
+        } else {
+          he = W.estart[v];
+          hc = W.estart[v] + W.planned[v] == W.lend[v];
+        }
+        const bool crit = tc && hc && te == he;
+        N.crit[k] = crit;
+        N.lo[k] = 0;
+        N.inf[k] = 1;
+        const long long fo = N.f[k];
+        if (crit) {
+          ++ninf;
+          max_inf_f = fo > max_inf_f ? fo : max_inf_f;
+        } else if (fo != 0) {
+          N.f[k] = 0;
+          flow_change(N, k, -fo);
+          ch = true;
+        }
       }
-      if (v == n + 1) {
-        he = t_cur;
-        hc = true;
-      } else {
-        he = W.estart[v];
-        hc = W.estart[v] + W.planned[v] == W.lend[v];
-      }
-      const bool crit = tc && hc && te == he;
-      N.ecrit[k] = crit;
-      N.lower[k] = 0;
-      N.einf[k] = 1;
-      N.cap[k] = 0;
-      N.flow[k] = 0;
-      if (crit) ++ninf;
-    }
-    if (ln == 0) {
-      N.ecrit[N.ret] = 0;
-      N.lower[N.ret] = 0;
-      N.einf[N.ret] = 0;
-      N.cap[N.ret] = 0;
-      N.flow[N.ret] = 0;
+      wappend(ch, ch ? N.tail[k] : 0, N.touch, ntouch);
+      wappend(ch, ch ? N.head[k] : 0, N.touch, ntouch);
     }
     suml = wsum128(suml);
     sumu = wsum128(sumu);
     ninf = wsum(ninf);
+    max_inf_f = wmax(max_inf_f);
     // infinity_sentinel (flow.hpp:58-68) and the aux total (flow.hpp:196-197)
     const i128 sent128 = suml + sumu + 1;
     if (sent128 > static_cast<i128>(LLONG_MAX / 4)) {
       status = PB_ERR_OVERFLOW;
       break;
     }
-    const long long sentinel = static_cast<long long>(sent128);
-    const i128 aux = sumu + static_cast<i128>(ninf) * sentinel + suml;
+    N.sentinel = static_cast<long long>(sent128);
+    const i128 aux = sumu + static_cast<i128>(ninf) * N.sentinel + suml;
     if (aux + 1 > static_cast<i128>(LLONG_MAX / 2)) {
       status = PB_ERR_OVERFLOW;
       break;
     }
     __syncwarp();
-    for (int k = ln; k < n + I.ne; k += 32)
-      if (N.ecrit[k] && N.einf[k]) N.cap[k] = sentinel - N.lower[k];
-    __syncwarp();
+    if (max_inf_f > N.sentinel) clamp_infinite(N, nedges, ntouch);
     C.add(kPrCap, now() - tcap);
-    // ---- K4 max flow with lower bounds
-    long long value = 0;
-    const int frc = solve_flow(N, static_cast<long long>(aux + 1), n_init, &value, C, &detail);
-    if (frc == 2) {
-      status = PB_ERR_LOGIC;
-      break;
-    }
-    if (frc) {
+    // ---- K4 warm-started max flow with lower bounds
+    if (!repair(N, ntouch, C)) {
       stop = PB_STOP_INFEASIBLE;
       break;
     }
-    if (value >= sentinel) {
-      clear_excess(N);
+    maximize(N, C);
+    if (N.f[N.ret] >= N.sentinel) {
       stop = PB_STOP_INFINITE_CUT;
       break;
     }
-    // ---- K5 minimal min cut
-    cut_bfs(N, C);
-    if (N.side[N.snk]) {
-      detail = 3;
-      status = PB_ERR_LOGIC;
-      break;
-    }
+    // ---- K5 minimal min cut = the last BFS's visited set
     const long long tupd = now();
-    clear_excess(N);
+    const int side_stamp = N.stamp;
     long long cost = 0;
     int nd = 0;
-    for (int base = 0; base < n + I.ne; base += 32) {
+    for (int base = 0; base < nedges; base += 32) {
       const int k = base + ln;
       int rec = 0;
-      if (k < n + I.ne && N.ecrit[k]) {
-        const int a = N.side[N.tail[k]], b = N.side[N.head[k]];
+      if (k < nedges && N.crit[k]) {
+        const bool a = N.vis[N.tail[k]] == side_stamp, b = N.vis[N.head[k]] == side_stamp;
         if (a && !b) {
-          cost += N.einf[k] ? sentinel : N.lower[k] + N.cap[k];
+          cost += N.inf[k] ? N.sentinel : N.up[k];
           if (k < n) rec = k + 1;
         } else if (!a && b) {
-          cost -= N.lower[k];
+          cost -= N.lo[k];
           if (k < n) {
             const int c = I.comp_class[k];
             if (!I.cls_const[c] && W.planned[k] + step <= I.cls_tmax[c]) rec = -(k + 1);
@@ -1003,24 +798,19 @@ struct WsPtrs {
 
 __device__ WsPtrs bind_ws(char* base, const WsLayout& L) {
   WsPtrs p;
-  p.N.excess = reinterpret_cast<int64_t*>(base + L.off_excess);
-  p.N.tres = reinterpret_cast<int64_t*>(base + L.off_tres);
-  p.N.height = reinterpret_cast<int32_t*>(base + L.off_height);
-  p.N.mark = reinterpret_cast<int32_t*>(base + L.off_mark);
-  p.N.nr = reinterpret_cast<uint8_t*>(base + L.off_nr);
-  p.N.side = reinterpret_cast<int32_t*>(base + L.off_side);
-  p.N.lower = reinterpret_cast<int64_t*>(base + L.off_lower);
-  p.N.cap = reinterpret_cast<int64_t*>(base + L.off_cap);
-  p.N.flow = reinterpret_cast<int64_t*>(base + L.off_flow);
-  p.N.einf = reinterpret_cast<uint8_t*>(base + L.off_einf);
-  p.N.ecrit = reinterpret_cast<uint8_t*>(base + L.off_ecrit);
-  p.N.list0 = reinterpret_cast<int32_t*>(base + L.off_list0);
-  p.N.list1 = reinterpret_cast<int32_t*>(base + L.off_list1);
-  p.N.bfs0 = reinterpret_cast<int32_t*>(base + L.off_bfs0);
-  p.N.bfs1 = reinterpret_cast<int32_t*>(base + L.off_bfs1);
-  p.N.dead = reinterpret_cast<int32_t*>(base + L.off_dead);
-  p.N.dem = reinterpret_cast<int32_t*>(base + L.off_dem);
-  p.N.tgt = reinterpret_cast<int32_t*>(base + L.off_tgt);
+  p.N.lo = reinterpret_cast<int64_t*>(base + L.off_lo);
+  p.N.up = reinterpret_cast<int64_t*>(base + L.off_up);
+  p.N.f = reinterpret_cast<int64_t*>(base + L.off_f);
+  p.N.inf = reinterpret_cast<uint8_t*>(base + L.off_inf);
+  p.N.crit = reinterpret_cast<uint8_t*>(base + L.off_crit);
+  p.N.bal = reinterpret_cast<int64_t*>(base + L.off_bal);
+  p.N.vis = reinterpret_cast<int32_t*>(base + L.off_vis);
+  p.N.par = reinterpret_cast<int32_t*>(base + L.off_par);
+  p.N.mk = reinterpret_cast<int32_t*>(base + L.off_mk);
+  p.N.f0 = reinterpret_cast<int32_t*>(base + L.off_f0);
+  p.N.f1 = reinterpret_cast<int32_t*>(base + L.off_f1);
+  p.N.touch = reinterpret_cast<int32_t*>(base + L.off_touch);
+  p.N.exl = reinterpret_cast<int32_t*>(base + L.off_exl);
   p.W.planned = reinterpret_cast<int64_t*>(base + L.off_planned);
   p.W.estart = reinterpret_cast<int64_t*>(base + L.off_estart);
   p.W.lend = reinterpret_cast<int64_t*>(base + L.off_lend);
@@ -1041,13 +831,8 @@ __device__ void flush_counters(const Counters& C, RunCounters* out) {
     atomicAdd(&out->arc_scans, a);
     atomicAdd(&out->node_updates, u);
     atomicAdd(&out->comp_visits, v);
-    atomicAdd(&out->rounds, C.rounds);
-    for (int q = 0; q < kPrSlots; ++q) {
-      if (q == kPrMaxRounds)
-        atomicMax(&out->prof[q], C.prof[q]);
-      else
-        atomicAdd(&out->prof[q], C.prof[q]);
-    }
+    atomicAdd(&out->rounds, C.prof[kPrBfsLevels]);
+    for (int q = 0; q < kPrSlots; ++q) atomicAdd(&out->prof[q], C.prof[q]);
   }
 }
 
@@ -1075,6 +860,8 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const DevInst* insts, int 
 
 // ------------------------------------------------------------ flow jobs
 
+// max_flow_lower_bounds + min_cut_from_flow on an arbitrary FlowGraph with
+// the same machinery from the all-lower-bound start (f = l everywhere).
 __global__ void __launch_bounds__(kBlock) flow_kernel(const DevFlowJob* jobs, int count,
                                                       char* ws_base, WsLayout L, int slots) {
   const int slot = warp_slot();
@@ -1094,50 +881,43 @@ __global__ void __launch_bounds__(kBlock) flow_kernel(const DevFlowJob* jobs, in
     N.inc = J.inc;
     N.tail = J.tail;
     N.head = J.head;
-    N.stamp = 1;
-    N.n_dead = 0;
-    N.n_dem = 0;
-    N.flag = 0;
-    for (int v = ln; v < N.V; v += 32) {
-      N.excess[v] = 0;
-      N.tres[v] = 0;
-      N.mark[v] = 0;
-      N.nr[v] = 0;
-      N.height[v] = 0;
-    }
+    reset_net(N);
     i128 suml = 0, sumu = 0;
     long long ninf = 0;
-    for (int e = ln; e < J.m; e += 32) {
-      N.lower[e] = J.lower[e];
-      N.einf[e] = J.inf[e];
-      N.ecrit[e] = 1;
-      N.flow[e] = 0;
-      suml += J.lower[e];
-      if (!J.inf[e])
-        sumu += J.upper[e];
-      else
-        ++ninf;
-    }
-    if (ln == 0) {
-      N.lower[N.ret] = 0;
-      N.einf[N.ret] = 0;
-      N.ecrit[N.ret] = 0;
-      N.flow[N.ret] = 0;
-      N.cap[N.ret] = 0;
+    int ntouch = 0;
+    for (int base = 0; base < J.m; base += 32) {
+      const int e = base + ln;
+      bool ch = false;
+      if (e < J.m) {
+        N.lo[e] = J.lower[e];
+        N.up[e] = J.upper[e];
+        N.inf[e] = J.inf[e];
+        N.crit[e] = 1;
+        suml += J.lower[e];
+        if (!J.inf[e])
+          sumu += J.upper[e];
+        else
+          ++ninf;
+        if (J.lower[e] > 0) {
+          N.f[e] = J.lower[e];
+          flow_change(N, e, J.lower[e]);
+          ch = true;
+        }
+      }
+      wappend(ch, ch ? J.tail[e] : 0, N.touch, ntouch);
+      wappend(ch, ch ? J.head[e] : 0, N.touch, ntouch);
     }
     suml = wsum128(suml);
     sumu = wsum128(sumu);
     ninf = wsum(ninf);
     const i128 sent128 = suml + sumu + 1;
     int status = PB_OK;
-    long long sentinel = 0;
     i128 aux = 0;
     if (sent128 > static_cast<i128>(LLONG_MAX / 4)) {
       status = PB_ERR_OVERFLOW;
     } else {
-      sentinel = static_cast<long long>(sent128);
-      // aux arcs: sum (resolved upper - lower) + sum lower_in + sum lower_out
-      aux = sumu + static_cast<i128>(ninf) * sentinel + suml;
+      N.sentinel = static_cast<long long>(sent128);
+      aux = sumu + static_cast<i128>(ninf) * N.sentinel + suml;
       if (aux + 1 > static_cast<i128>(LLONG_MAX / 2)) status = PB_ERR_OVERFLOW;
     }
     __syncwarp();
@@ -1149,49 +929,23 @@ __global__ void __launch_bounds__(kBlock) flow_kernel(const DevFlowJob* jobs, in
       __syncwarp();
       continue;
     }
-    for (int e = ln; e < J.m; e += 32) N.cap[e] = (J.inf[e] ? sentinel : J.upper[e]) - J.lower[e];
-    __syncwarp();
-    // netted demands per node
-    int n_init = 0;
-    for (int base = 0; base < N.V; base += 32) {
-      const int v = base + ln;
-      long long d = 0;
-      if (v < N.V)
-        for (int j = N.inc_off[v]; j < N.inc_off[v + 1]; ++j) {
-          const int a = N.inc[j];
-          const int ed = a >> 1;
-          if (ed == N.ret) continue;
-          d += (a & 1) ? N.lower[ed] : -N.lower[ed];
-        }
-      if (d > 0) N.excess[v] = d;
-      if (d < 0) N.tres[v] = -d;
-      wappend(d > 0, v, N.list0, n_init);
-      wappend(d < 0, v, N.dem, N.n_dem);
-    }
-    __syncwarp();
-    long long value = 0;
-    int detail = 0;
-    const int frc = solve_flow(N, static_cast<long long>(aux + 1), n_init, &value, C, &detail);
-    if (frc) {
-      for (int v = ln; v < N.V; v += 32) {
-        N.excess[v] = 0;
-        N.tres[v] = 0;
-      }
+    if (!repair(N, ntouch, C)) {
       if (ln == 0) {
-        J.status[g] = frc == 2 ? PB_ERR_LOGIC : PB_OK;
+        J.status[g] = PB_OK;
         J.feasible[g] = 0;
-        J.sentinel[g] = sentinel;
+        J.sentinel[g] = N.sentinel;
       }
       __syncwarp();
       continue;
     }
-    cut_bfs(N, C);
+    maximize(N, C);
+    const int side_stamp = N.stamp;
     long long cost = 0;
     for (int e = ln; e < J.m; e += 32) {
-      const int a = N.side[N.tail[e]], b = N.side[N.head[e]];
+      const bool a = N.vis[N.tail[e]] == side_stamp, b = N.vis[N.head[e]] == side_stamp;
       int8_t dir = 0;
       if (a && !b) {
-        cost += J.inf[e] ? sentinel : J.upper[e];
+        cost += J.inf[e] ? N.sentinel : J.upper[e];
         dir = 1;
       } else if (!a && b) {
         cost -= J.lower[e];
@@ -1199,16 +953,16 @@ __global__ void __launch_bounds__(kBlock) flow_kernel(const DevFlowJob* jobs, in
       }
       J.cut_dir[e] = dir;
     }
-    for (int v = ln; v < N.V; v += 32) J.side[v] = static_cast<uint8_t>(N.side[v]);
+    for (int v = ln; v < N.V; v += 32) J.side[v] = N.vis[v] == side_stamp ? 1 : 0;
     cost = wsum(cost);
     if (ln == 0) {
-      J.status[g] = N.side[N.snk] ? PB_ERR_LOGIC : PB_OK;
+      J.status[g] = N.vis[N.snk] == side_stamp ? PB_ERR_LOGIC : PB_OK;
       J.feasible[g] = 1;
-      J.value[g] = value;
-      J.sentinel[g] = sentinel;
+      J.value[g] = N.f[N.ret];
+      J.sentinel[g] = N.sentinel;
       J.cost[g] = cost;
     }
-    clear_excess(N);
+    __syncwarp();
   }
 }
 

@@ -13,8 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2312_06902_b200 as pb  # noqa: E402
 from paper_2312_06902_b200 import _native as N, g9  # noqa: E402
 
-NAMES = ["lp", "cap", "phaseA", "phaseB", "gr", "cut", "update", "walk", "gr_calls", "gr_levels",
-         "cut_levels", "rounds_A", "rounds_B", "steps", "max_rounds", "lp_levels"]
+NAMES = ["lp", "cap", "phaseA", "phaseB", "bfs", "augment", "update", "walk", "bfs_A", "bfs_B",
+         "bfs_levels", "paths", "path_hops", "steps", "imbalanced", "lp_levels"]
 
 
 def profile(name):
@@ -37,8 +37,8 @@ def profile(name):
     print(f"== {name}: kernel {ms:.1f} ms, {steps} steps, {ms * 1e3 / max(steps, 1):.1f} us/step, wall {time.time() - t:.1f}s")
     print("   cycles share: " + ", ".join(f"{NAMES[i]} {prof[i] / walk:.1%}" for i in range(7)))
     S = max(prof[13], 1)
-    print("   per step: " + ", ".join(f"{NAMES[i]} {prof[i] / S:.1f}" for i in range(8, 16) if i != 14)
-          + f", max_rounds(one call) {prof[14]}")
+    print("   per step: " + ", ".join(f"{NAMES[i]} {prof[i] / S:.2f}" for i in range(8, 16)))
+    print(f"   cycles/step {prof[7] / S:.0f}, cycles per bfs level {prof[4] / max(prof[10], 1):.0f}")
     print(f"   arc_scans/step {st.arc_scans / S:.0f}, node_updates/step {st.node_updates / S:.0f}")
     if bad:
         print("   FAILED (index, status, detail, steps):", bad[:10])
