@@ -51,43 +51,74 @@ struct HostInst {
   int64_t quantum = 1, tau = 1000;
   std::vector<int64_t> start;  // empty = min-energy seed
   int32_t max_steps = 0;
-  // derived by validate()
+  // derived by validate_and_derive(): the static device layout (pb_internal.h)
   int32_t n_levels = 0;
-  std::vector<int32_t> lvl_off, lvl_comps, in_off, in_dep, out_off, out_dep, snk_dep;
-  std::vector<int32_t> inc_off, inc, ec_tail, ec_head;
+  std::vector<int32_t> lvl_off, orig, inv, icls;
+  std::vector<uint8_t> cflag;
+  std::vector<int32_t> pin_off, pin, pout_off, pout;
+  std::vector<pb::int4h> frow, brow;
+  std::vector<pb::int2h> dep_nd;
+  pb::NetLayout net;
+  std::vector<int64_t> istart;  // start schedule in internal order
   int64_t t_min_est = 0, t_star_est = 0, est_steps = 0, work = 0;
 };
 
-// Longest path on the node DAG with the given durations (host estimate used
-// only to size output buffers and order work; the device computes its own).
+// Longest path on the node DAG with the given durations (internal order;
+// host estimate used only to size output buffers and order work; the device
+// computes its own).
 int64_t host_makespan(const HostInst& h, const std::vector<int64_t>& dur) {
-  std::vector<int64_t> start(h.n, 0);
-  for (int32_t L = 0; L < h.n_levels; ++L)
-    for (int32_t q = h.lvl_off[L]; q < h.lvl_off[L + 1]; ++q) {
-      const int32_t i = h.lvl_comps[q];
-      int64_t m = 0;
-      for (int32_t j = h.in_off[i]; j < h.in_off[i + 1]; ++j) {
-        const int32_t u = h.edge_tail[h.in_dep[j]];
-        if (u < h.n) m = std::max(m, start[u] + dur[u]);
-      }
-      start[i] = m;
-    }
+  std::vector<int64_t> fin(h.n, 0);
   int64_t ms = 0;
-  for (int32_t j : h.snk_dep) {
-    const int32_t u = h.edge_tail[j];
-    if (u < h.n) ms = std::max(ms, start[u] + dur[u]);
+  for (int32_t i = 0; i < h.n; ++i) {
+    int64_t m = 0;
+    for (int32_t j = h.pin_off[i]; j < h.pin_off[i + 1]; ++j) m = std::max(m, fin[h.pin[j]]);
+    fin[i] = m + dur[i];
+    if (h.cflag[i] & 2) ms = std::max(ms, fin[i]);
   }
   return ms;
 }
 
+}  // namespace
+
+namespace pb {
+// Position-indexed incidence of an edge list (tail[k] -> head[k], k < E):
+// per node the list of its arcs; entry p = {other end, twin position,
+// other's list range}; epos[k] = {position at tail, position at head}.
+void build_net(int32_t V, const std::vector<int32_t>& tail, const std::vector<int32_t>& head,
+               NetLayout& out) {
+  const int32_t E = static_cast<int32_t>(tail.size());
+  out.inc_off.assign(V + 1, 0);
+  for (int32_t k = 0; k < E; ++k) {
+    ++out.inc_off[tail[k] + 1];
+    ++out.inc_off[head[k] + 1];
+  }
+  for (int32_t v = 0; v < V; ++v) out.inc_off[v + 1] += out.inc_off[v];
+  out.epos.assign(E, int2h{0, 0});
+  std::vector<int32_t> fill(out.inc_off.begin(), out.inc_off.end() - 1);
+  for (int32_t k = 0; k < E; ++k) {
+    out.epos[k].x = fill[tail[k]]++;
+    out.epos[k].y = fill[head[k]]++;
+  }
+  out.ient.assign(out.inc_off[V], IEnt{0, 0, 0, 0});
+  for (int32_t k = 0; k < E; ++k) {
+    const int32_t a = tail[k], b = head[k], pa = out.epos[k].x, pb = out.epos[k].y;
+    out.ient[pa] = IEnt{b, pb, out.inc_off[b], out.inc_off[b + 1]};
+    out.ient[pb] = IEnt{a, pa, out.inc_off[a], out.inc_off[a + 1]};
+  }
+}
+}  // namespace pb
+
+namespace {
+
 // Validation mirrors the reference's throws; derived arrays are the static
-// device layout (levels, CSRs, edge-centric incidence).
+// device layout (level-major computations, row records, incidence).
 pb_status validate_and_derive(HostInst& h) {
   const int32_t n = h.n, ne = static_cast<int32_t>(h.edge_tail.size());
   const int32_t nc = static_cast<int32_t>(h.cls_const.size());
   if (n < 1) return fail(PB_ERR_INVALID_ARGUMENT, "dag needs at least one computation");
   if (h.tau <= 0) return fail(PB_ERR_INVALID_ARGUMENT, "tau must be positive");
   if (h.quantum <= 0) return fail(PB_ERR_INVALID_ARGUMENT, "quantum must be positive");
+  if (n > (1 << 28)) return fail(PB_ERR_UNSUPPORTED, "too many computations");
   for (int32_t c = 0; c < nc; ++c) {
     const int32_t np = h.cls_pt_off[c + 1] - h.cls_pt_off[c];
     if (np < 1) return fail(PB_ERR_INVALID_ARGUMENT, "profile has no points");
@@ -138,65 +169,75 @@ pb_status validate_and_derive(HostInst& h) {
   h.lvl_off.assign(L + 1, 0);
   for (int32_t i = 0; i < n; ++i) ++h.lvl_off[level[i] + 1];
   for (int32_t l = 0; l < L; ++l) h.lvl_off[l + 1] += h.lvl_off[l];
-  h.lvl_comps.assign(n, 0);
+  // level-major renumbering (stable in caller order inside a level)
+  h.orig.assign(n, 0);
+  h.inv.assign(n, 0);
   {
     std::vector<int32_t> fill(h.lvl_off.begin(), h.lvl_off.end() - 1);
-    for (int32_t i = 0; i < n; ++i) h.lvl_comps[fill[level[i]]++] = i;
-  }
-  auto csr = [&](bool by_head, std::vector<int32_t>& off, std::vector<int32_t>& idx) {
-    off.assign(n + 1, 0);
-    for (int32_t j = 0; j < ne; ++j) {
-      const int32_t x = by_head ? h.edge_head[j] : h.edge_tail[j];
-      if (x < n) ++off[x + 1];
+    for (int32_t i = 0; i < n; ++i) {
+      h.inv[i] = fill[level[i]]++;
+      h.orig[h.inv[i]] = i;
     }
-    for (int32_t i = 0; i < n; ++i) off[i + 1] += off[i];
-    idx.assign(off[n], 0);
-    std::vector<int32_t> fill(off.begin(), off.end() - 1);
-    for (int32_t j = 0; j < ne; ++j) {
-      const int32_t x = by_head ? h.edge_head[j] : h.edge_tail[j];
-      if (x < n) idx[fill[x]++] = j;
+  }
+  auto in_id = [&](int32_t x) { return x < n ? h.inv[x] : x; };
+  h.icls.assign(n, 0);
+  for (int32_t i = 0; i < n; ++i) h.icls[h.inv[i]] = h.comp_class[i];
+  h.cflag.assign(n, 0);
+  h.dep_nd.assign(ne, pb::int2h{0, 0});
+  std::vector<std::vector<int32_t>> pv(n), sv(n);
+  for (int32_t j = 0; j < ne; ++j) {
+    const int32_t u = in_id(h.edge_tail[j]), v = in_id(h.edge_head[j]);
+    h.dep_nd[j] = pb::int2h{u, v};
+    if (v == n + 1 && u < n) h.cflag[u] |= 2;
+    if (u == n && v < n) h.cflag[v] |= 1;
+    if (u < n && v < n) {
+      pv[v].push_back(u);
+      sv[u].push_back(v);
+    }
+  }
+  auto csr = [&](std::vector<std::vector<int32_t>>& lists, std::vector<int32_t>& off,
+                 std::vector<int32_t>& idx, std::vector<pb::int4h>& row, bool with_sink) {
+    off.assign(n + 1, 0);
+    idx.clear();
+    row.assign(n, pb::int4h{0, -1, -1, -1});
+    for (int32_t i = 0; i < n; ++i) {
+      const auto& l = lists[i];
+      const int32_t c = static_cast<int32_t>(l.size());
+      row[i].x = std::min(c, 0xffff) | (with_sink && (h.cflag[i] & 2) ? (1 << 16) : 0);
+      if (c > 0) row[i].y = l[0];
+      if (c > 1) row[i].z = l[1];
+      if (c > 2) row[i].w = l[2];
+      idx.insert(idx.end(), l.begin(), l.end());
+      off[i + 1] = static_cast<int32_t>(idx.size());
     }
   };
-  csr(true, h.in_off, h.in_dep);
-  csr(false, h.out_off, h.out_dep);
-  h.snk_dep.clear();
-  for (int32_t j = 0; j < ne; ++j)
-    if (h.edge_head[j] == n + 1) h.snk_dep.push_back(j);
-  // edge-centric graph (dag.hpp:209-224) + return arc
-  const int32_t V = 2 * n + 2, E = n + ne + 1;
-  h.ec_tail.assign(E, 0);
-  h.ec_head.assign(E, 0);
+  csr(pv, h.pin_off, h.pin, h.frow, true);
+  csr(sv, h.pout_off, h.pout, h.brow, false);
+  // edge-centric network (dag.hpp:209-224) + return arc, internal ids
+  const int32_t V = 2 * n + 2;
+  std::vector<int32_t> et(n + ne + 1), eh(n + ne + 1);
   for (int32_t i = 0; i < n; ++i) {
-    h.ec_tail[i] = 2 * i;
-    h.ec_head[i] = 2 * i + 1;
+    et[i] = 2 * i;
+    eh[i] = 2 * i + 1;
   }
   for (int32_t j = 0; j < ne; ++j) {
-    const int32_t u = h.edge_tail[j], v = h.edge_head[j];
-    h.ec_tail[n + j] = u == n ? 2 * n : 2 * u + 1;
-    h.ec_head[n + j] = v == n + 1 ? 2 * n + 1 : 2 * v;
+    const int32_t u = h.dep_nd[j].x, v = h.dep_nd[j].y;
+    et[n + j] = u == n ? 2 * n : 2 * u + 1;
+    eh[n + j] = v == n + 1 ? 2 * n + 1 : 2 * v;
   }
-  h.ec_tail[n + ne] = 2 * n + 1;
-  h.ec_head[n + ne] = 2 * n;
-  h.inc_off.assign(V + 1, 0);
-  for (int32_t k = 0; k < E; ++k) {
-    ++h.inc_off[h.ec_tail[k] + 1];
-    ++h.inc_off[h.ec_head[k] + 1];
-  }
-  for (int32_t v = 0; v < V; ++v) h.inc_off[v + 1] += h.inc_off[v];
-  h.inc.assign(h.inc_off[V], 0);
-  {
-    std::vector<int32_t> fill(h.inc_off.begin(), h.inc_off.end() - 1);
-    for (int32_t k = 0; k < E; ++k) {
-      h.inc[fill[h.ec_tail[k]]++] = k << 1;
-      h.inc[fill[h.ec_head[k]]++] = (k << 1) | 1;
-    }
+  et[n + ne] = 2 * n + 1;
+  eh[n + ne] = 2 * n;
+  pb::build_net(V, et, eh, h.net);
+  if (!h.start.empty()) {
+    h.istart.assign(n, 0);
+    for (int32_t i = 0; i < n; ++i) h.istart[h.inv[i]] = h.start[i];
   }
   // sizing estimates
   std::vector<int64_t> fast(n), seed(n);
   for (int32_t i = 0; i < n; ++i) {
-    const int32_t c = h.comp_class[i];
+    const int32_t c = h.icls[i];
     fast[i] = h.pt_time[h.cls_pt_off[c]];
-    seed[i] = h.start.empty() ? (h.cls_const[c] ? fast[i] : h.cls_trange[2 * c + 1]) : h.start[i];
+    seed[i] = h.start.empty() ? (h.cls_const[c] ? fast[i] : h.cls_trange[2 * c + 1]) : h.istart[i];
   }
   h.t_min_est = host_makespan(h, fast);
   h.t_star_est = host_makespan(h, seed);
@@ -207,7 +248,7 @@ pb_status validate_and_derive(HostInst& h) {
     h.est_steps = gap / h.tau + 2;
     if (h.max_steps > 0) h.est_steps = std::min<int64_t>(h.est_steps, h.max_steps);
   }
-  h.work = static_cast<int64_t>(E) * h.est_steps;
+  h.work = static_cast<int64_t>(n + ne + 1) * h.est_steps;
   return PB_OK;
 }
 
@@ -225,6 +266,10 @@ struct Blob {
   size_t put(const std::vector<T>& v) {
     return put(v.data(), v.size() * sizeof(T));
   }
+};
+
+struct int2h_pair {
+  int32_t a, b;
 };
 
 struct CurveKey {
@@ -318,10 +363,37 @@ struct Packed {
 };
 
 enum OffIdx {
-  O_CLASS, O_LVLOFF, O_LVL, O_INOFF, O_INDEP, O_OUTOFF, O_OUTDEP, O_SNK, O_DTAIL, O_DHEAD,
-  O_INCOFF, O_INC, O_ECT, O_ECH, O_CCONST, O_CTMIN, O_CTMAX, O_CTAB, O_CPOFF, O_PTIME, O_PENERGY,
+  O_ORIG, O_CLASS, O_CFLAG, O_LVLOFF, O_FROW, O_BROW, O_PINOFF, O_PIN, O_POUTOFF, O_POUT, O_DEPND,
+  O_INCOFF, O_IENT, O_EPOS, O_CCONST, O_CTMIN, O_CTMAX, O_CTAB, O_CPOFF, O_PTIME, O_PENERGY,
   O_START, O_CURVE, O_POINTS, O_SUMMARY, O_COUNT
 };
+
+void put_static(Blob& blob, const HostInst& h, std::array<size_t, 32>& o) {
+  o[O_ORIG] = blob.put(h.orig);
+  o[O_CLASS] = blob.put(h.icls);
+  o[O_CFLAG] = blob.put(h.cflag);
+  o[O_LVLOFF] = blob.put(h.lvl_off);
+  o[O_FROW] = blob.put(h.frow);
+  o[O_BROW] = blob.put(h.brow);
+  o[O_PINOFF] = blob.put(h.pin_off);
+  o[O_PIN] = blob.put(h.pin);
+  o[O_POUTOFF] = blob.put(h.pout_off);
+  o[O_POUT] = blob.put(h.pout);
+  o[O_DEPND] = blob.put(h.dep_nd);
+  o[O_INCOFF] = blob.put(h.net.inc_off);
+  o[O_IENT] = blob.put(h.net.ient);
+  o[O_EPOS] = blob.put(h.net.epos);
+}
+
+void fill_shape(pb::DevInst& d, const HostInst& h) {
+  d.n = h.n;
+  d.ne = static_cast<int32_t>(h.edge_tail.size());
+  d.n_levels = h.n_levels;
+  d.V = 2 * h.n + 2;
+  d.E = h.n + d.ne + 1;
+  d.ret_pt = h.net.epos[d.E - 1].x;
+  d.ret_ph = h.net.epos[d.E - 1].y;
+}
 
 void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_scale) {
   const size_t N = b->insts.size();
@@ -366,34 +438,20 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
   for (size_t k = 0; k < N; ++k) {
     const HostInst& h = b->insts[k];
     auto& o = P.offs[k];
-    std::vector<uint8_t> cconst = h.cls_const;
     std::vector<int64_t> tmin(h.cls_const.size()), tmax(h.cls_const.size());
     for (size_t c = 0; c < h.cls_const.size(); ++c) {
       tmin[c] = h.cls_trange[2 * c];
       tmax[c] = h.cls_trange[2 * c + 1];
     }
-    o[O_CLASS] = P.stat.put(h.comp_class);
-    o[O_LVLOFF] = P.stat.put(h.lvl_off);
-    o[O_LVL] = P.stat.put(h.lvl_comps);
-    o[O_INOFF] = P.stat.put(h.in_off);
-    o[O_INDEP] = P.stat.put(h.in_dep);
-    o[O_OUTOFF] = P.stat.put(h.out_off);
-    o[O_OUTDEP] = P.stat.put(h.out_dep);
-    o[O_SNK] = P.stat.put(h.snk_dep);
-    o[O_DTAIL] = P.stat.put(h.edge_tail);
-    o[O_DHEAD] = P.stat.put(h.edge_head);
-    o[O_INCOFF] = P.stat.put(h.inc_off);
-    o[O_INC] = P.stat.put(h.inc);
-    o[O_ECT] = P.stat.put(h.ec_tail);
-    o[O_ECH] = P.stat.put(h.ec_head);
-    o[O_CCONST] = P.stat.put(cconst);
+    put_static(P.stat, h, o);
+    o[O_CCONST] = P.stat.put(h.cls_const);
     o[O_CTMIN] = P.stat.put(tmin);
     o[O_CTMAX] = P.stat.put(tmax);
     o[O_CTAB] = P.stat.put(b->cls_tab[k]);
     o[O_CPOFF] = P.stat.put(h.cls_pt_off);
     o[O_PTIME] = P.stat.put(h.pt_time);
     o[O_PENERGY] = P.stat.put(h.pt_energy);
-    o[O_START] = h.start.empty() ? SIZE_MAX : P.stat.put(h.start);
+    o[O_START] = h.istart.empty() ? SIZE_MAX : P.stat.put(h.istart);
     o[O_CURVE] = P.stat.put(h.cls_curve);
     const int64_t est = static_cast<int64_t>(static_cast<double>(h.est_steps) * cap_scale);
     cap_points[k] = static_cast<int32_t>(std::min<int64_t>(est + 8, INT32_MAX / 2));
@@ -401,20 +459,16 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
     o[O_POINTS] = out_take(sizeof(pb_point) * cap_points[k]);
     o[O_SUMMARY] = out_take(sizeof(pb_frontier_summary));
     pb::DevInst& d = P.dev[k];
-    d.n = h.n;
-    d.ne = static_cast<int32_t>(h.edge_tail.size());
-    d.n_levels = h.n_levels;
+    fill_shape(d, h);
     d.mode = h.start.empty() ? pb::kModeDiscover : pb::kModeGetNext;
     d.max_steps = h.start.empty() ? h.max_steps : (h.max_steps == 0 ? 1 : h.max_steps);
     d.cap_points = cap_points[k];
-    d.cap_ids = 0;
     d.tau = h.tau;
     d.watts = h.watts;
     d.quantum = h.quantum;
-    d.n_snk = static_cast<int32_t>(h.snk_dep.size());
-    P.max_n = std::max<int64_t>(P.max_n, h.n);
-    P.max_v = std::max<int64_t>(P.max_v, 2 * int64_t{h.n} + 2);
-    P.max_e = std::max<int64_t>(P.max_e, h.n + static_cast<int64_t>(h.edge_tail.size()) + 1);
+    P.max_n = std::max<int64_t>(P.max_n, d.n);
+    P.max_v = std::max<int64_t>(P.max_v, d.V);
+    P.max_e = std::max<int64_t>(P.max_e, d.E);
   }
   P.out_bytes = out;
   P.pool_cap = std::min<long long>(pool, (1ll << 31) - 1);
@@ -441,24 +495,28 @@ T* dptr(char* base, size_t off) {
   return off == SIZE_MAX ? nullptr : reinterpret_cast<T*>(base + off);
 }
 
+void bind_static(pb::DevInst& d, char* base, const std::array<size_t, 32>& o) {
+  d.orig = dptr<int32_t>(base, o[O_ORIG]);
+  d.comp_class = dptr<int32_t>(base, o[O_CLASS]);
+  d.cflag = dptr<uint8_t>(base, o[O_CFLAG]);
+  d.lvl_off = dptr<int32_t>(base, o[O_LVLOFF]);
+  d.frow = dptr<int4>(base, o[O_FROW]);
+  d.brow = dptr<int4>(base, o[O_BROW]);
+  d.pin_off = dptr<int32_t>(base, o[O_PINOFF]);
+  d.pin = dptr<int32_t>(base, o[O_PIN]);
+  d.pout_off = dptr<int32_t>(base, o[O_POUTOFF]);
+  d.pout = dptr<int32_t>(base, o[O_POUT]);
+  d.dep_nd = dptr<int2>(base, o[O_DEPND]);
+  d.inc_off = dptr<int32_t>(base, o[O_INCOFF]);
+  d.ient = dptr<pb::IEnt>(base, o[O_IENT]);
+  d.epos = dptr<int2>(base, o[O_EPOS]);
+}
+
 void bind_device(Packed& P, char* d_static, char* d_out, size_t tables_off) {
   for (size_t k = 0; k < P.dev.size(); ++k) {
     auto& o = P.offs[k];
     pb::DevInst& d = P.dev[k];
-    d.comp_class = dptr<int32_t>(d_static, o[O_CLASS]);
-    d.lvl_off = dptr<int32_t>(d_static, o[O_LVLOFF]);
-    d.lvl_comps = dptr<int32_t>(d_static, o[O_LVL]);
-    d.in_off = dptr<int32_t>(d_static, o[O_INOFF]);
-    d.in_dep = dptr<int32_t>(d_static, o[O_INDEP]);
-    d.out_off = dptr<int32_t>(d_static, o[O_OUTOFF]);
-    d.out_dep = dptr<int32_t>(d_static, o[O_OUTDEP]);
-    d.snk_dep = dptr<int32_t>(d_static, o[O_SNK]);
-    d.dep_tail = dptr<int32_t>(d_static, o[O_DTAIL]);
-    d.dep_head = dptr<int32_t>(d_static, o[O_DHEAD]);
-    d.inc_off = dptr<int32_t>(d_static, o[O_INCOFF]);
-    d.inc = dptr<int32_t>(d_static, o[O_INC]);
-    d.ec_tail = dptr<int32_t>(d_static, o[O_ECT]);
-    d.ec_head = dptr<int32_t>(d_static, o[O_ECH]);
+    bind_static(d, d_static, o);
     d.cls_const = dptr<uint8_t>(d_static, o[O_CCONST]);
     d.cls_tmin = dptr<int64_t>(d_static, o[O_CTMIN]);
     d.cls_tmax = dptr<int64_t>(d_static, o[O_CTMAX]);
@@ -474,10 +532,10 @@ void bind_device(Packed& P, char* d_static, char* d_out, size_t tables_off) {
   }
 }
 
-int32_t device_slots(int device, int64_t n_inst) {
+int32_t device_slots(int device, int64_t n_inst, const pb::WsLayout& ws) {
   int sms = 0;
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
-  const int per_sm = std::max(1, pb::walk_slots_per_sm());
+  const int per_sm = std::max(1, pb::walk_slots_per_sm(ws));
   return static_cast<int32_t>(std::min<int64_t>(n_inst, int64_t{sms} * per_sm));
 }
 
@@ -505,7 +563,7 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   ck(cudaMallocHost(&R.h_out, R.out_bytes), "malloc pinned out");
   bind_device(P, R.d_static, R.d_out, tables_off);
   R.ws = pb::make_ws_layout(P.max_n, P.max_v, P.max_e);
-  R.slots = device_slots(device, static_cast<int64_t>(N));
+  R.slots = device_slots(device, static_cast<int64_t>(N), R.ws);
   ck(cudaMalloc(&R.d_ws, static_cast<size_t>(R.ws.stride) * R.slots), "malloc workspace");
   ck(cudaMalloc(&R.d_insts, sizeof(pb::DevInst) * N), "malloc insts");
   ck(cudaMalloc(&R.d_order, sizeof(int32_t) * N), "malloc order");
@@ -1029,30 +1087,24 @@ pb_status pb_annotate_slack_batch(int32_t device, int32_t count, const int32_t* 
     }
     ck(cudaSetDevice(device), "cudaSetDevice");
     Blob blob;
-    std::vector<std::array<size_t, 8>> off(count);
-    size_t out_e = 0, out_l = 0, out_c = 0;
-    std::vector<size_t> o_e(count), o_l(count), o_c(count), o_d(count);
+    std::vector<std::array<size_t, 32>> off(count);
+    size_t out_e = 0, out_c = 0;
+    std::vector<size_t> o_e(count), o_c(count), o_d(count);
     int64_t max_n = 1, max_v = 1, max_e = 1;
     dofs = 0;
     for (int32_t g = 0; g < count; ++g) {
       const HostInst& h = hs[g];
-      off[g] = {blob.put(h.lvl_off), blob.put(h.lvl_comps), blob.put(h.in_off), blob.put(h.in_dep),
-                blob.put(h.out_off), blob.put(h.out_dep), blob.put(h.snk_dep), 0};
-      off[g][7] = blob.put(h.edge_tail);
+      put_static(blob, h, off[g]);
       o_d[g] = blob.put(durations + dofs, sizeof(int64_t) * h.n);
       dofs += h.n;
       o_e[g] = out_e;
-      o_l[g] = out_l;
       out_e += 2 * h.n + 2;
-      out_l += 2 * h.n + 2;
       o_c[g] = out_c;
       out_c += h.n + h.edge_tail.size();
       max_n = std::max<int64_t>(max_n, h.n);
       max_v = std::max<int64_t>(max_v, 2 * int64_t{h.n} + 2);
       max_e = std::max<int64_t>(max_e, h.n + static_cast<int64_t>(h.edge_tail.size()) + 1);
     }
-    std::vector<size_t> o_h(count);
-    for (int32_t g = 0; g < count; ++g) o_h[g] = blob.put(hs[g].edge_head);
     char *d_blob = nullptr, *d_ws = nullptr;
     int64_t *d_e = nullptr, *d_l = nullptr, *d_ms = nullptr;
     uint8_t* d_c = nullptr;
@@ -1062,7 +1114,7 @@ pb_status pb_annotate_slack_batch(int32_t device, int32_t count, const int32_t* 
     const int32_t slots = std::min<int32_t>(count, 1024);
     ck(cudaMalloc(&d_blob, std::max<size_t>(blob.bytes.size(), 256)), "malloc");
     ck(cudaMalloc(&d_e, sizeof(int64_t) * out_e), "malloc");
-    ck(cudaMalloc(&d_l, sizeof(int64_t) * out_l), "malloc");
+    ck(cudaMalloc(&d_l, sizeof(int64_t) * out_e), "malloc");
     ck(cudaMalloc(&d_c, std::max<size_t>(out_c, 1)), "malloc");
     ck(cudaMalloc(&d_ms, sizeof(int64_t) * count), "malloc");
     ck(cudaMalloc(&d_ws, static_cast<size_t>(ws.stride) * slots), "malloc");
@@ -1074,22 +1126,11 @@ pb_status pb_annotate_slack_batch(int32_t device, int32_t count, const int32_t* 
     for (int32_t g = 0; g < count; ++g) {
       const HostInst& h = hs[g];
       pb::DevInst& d = di[g];
-      d.n = h.n;
-      d.ne = static_cast<int32_t>(h.edge_tail.size());
-      d.n_levels = h.n_levels;
-      d.lvl_off = dptr<int32_t>(d_blob, off[g][0]);
-      d.lvl_comps = dptr<int32_t>(d_blob, off[g][1]);
-      d.in_off = dptr<int32_t>(d_blob, off[g][2]);
-      d.in_dep = dptr<int32_t>(d_blob, off[g][3]);
-      d.out_off = dptr<int32_t>(d_blob, off[g][4]);
-      d.out_dep = dptr<int32_t>(d_blob, off[g][5]);
-      d.snk_dep = dptr<int32_t>(d_blob, off[g][6]);
-      d.n_snk = static_cast<int32_t>(h.snk_dep.size());
-      d.dep_tail = dptr<int32_t>(d_blob, off[g][7]);
-      d.dep_head = dptr<int32_t>(d_blob, o_h[g]);
+      fill_shape(d, h);
+      bind_static(d, d_blob, off[g]);
       so[g].dur = dptr<int64_t>(d_blob, o_d[g]);
       so[g].earliest = d_e + o_e[g];
-      so[g].latest = d_l + o_l[g];
+      so[g].latest = d_l + o_e[g];
       so[g].critical = d_c + o_c[g];
     }
     ck(cudaMemcpy(d_insts, di.data(), sizeof(pb::DevInst) * count, cudaMemcpyHostToDevice), "H2D");
@@ -1098,7 +1139,7 @@ pb_status pb_annotate_slack_batch(int32_t device, int32_t count, const int32_t* 
     if (rc) throw CudaError(cudaGetErrorString(static_cast<cudaError_t>(rc)));
     ck(cudaDeviceSynchronize(), "slack kernel");
     ck(cudaMemcpy(earliest, d_e, sizeof(int64_t) * out_e, cudaMemcpyDeviceToHost), "D2H");
-    ck(cudaMemcpy(latest, d_l, sizeof(int64_t) * out_l, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(latest, d_l, sizeof(int64_t) * out_e, cudaMemcpyDeviceToHost), "D2H");
     ck(cudaMemcpy(critical, d_c, out_c, cudaMemcpyDeviceToHost), "D2H");
     ck(cudaMemcpy(makespan, d_ms, sizeof(int64_t) * count, cudaMemcpyDeviceToHost), "D2H");
     cudaFree(d_blob);
@@ -1140,7 +1181,8 @@ pb_status pb_flow_min_cut_batch(int32_t device, int32_t count, const int32_t* no
     }
     ck(cudaSetDevice(device), "cudaSetDevice");
     Blob blob;
-    std::vector<std::array<size_t, 7>> off(count);
+    std::vector<std::array<size_t, 8>> off(count);
+    std::vector<int2h_pair> rets(count);
     int64_t max_v = 2, max_e = 1;
     eo = 0;
     for (int32_t g = 0; g < count; ++g) {
@@ -1148,24 +1190,19 @@ pb_status pb_flow_min_cut_batch(int32_t device, int32_t count, const int32_t* no
       std::vector<int32_t> t(tail + eo, tail + eo + M), h(head + eo, head + eo + M);
       t.push_back(sink[g]);
       h.push_back(source[g]);
-      std::vector<int32_t> io(V + 1, 0), inc(2 * (M + 1));
-      for (int32_t k = 0; k <= M; ++k) {
-        ++io[t[k] + 1];
-        ++io[h[k] + 1];
-      }
-      for (int32_t v = 0; v < V; ++v) io[v + 1] += io[v];
-      std::vector<int32_t> fill(io.begin(), io.end() - 1);
-      for (int32_t k = 0; k <= M; ++k) {
-        inc[fill[t[k]]++] = k << 1;
-        inc[fill[h[k]]++] = (k << 1) | 1;
-      }
-      off[g][0] = blob.put(io);
-      off[g][1] = blob.put(inc);
+      pb::NetLayout net;
+      pb::build_net(V, t, h, net);
+      rets[g] = {net.epos[M].x, net.epos[M].y};
+      t.pop_back();
+      h.pop_back();
+      off[g][0] = blob.put(net.inc_off);
+      off[g][1] = blob.put(net.ient);
       off[g][2] = blob.put(t);
       off[g][3] = blob.put(h);
       off[g][4] = blob.put(lower + eo, sizeof(int64_t) * M);
       off[g][5] = blob.put(upper + eo, sizeof(int64_t) * M);
       off[g][6] = blob.put(infinite + eo, M);
+      off[g][7] = blob.put(net.epos);
       max_v = std::max<int64_t>(max_v, V);
       max_e = std::max<int64_t>(max_e, M + 1);
       eo += M;
@@ -1197,7 +1234,10 @@ pb_status pb_flow_min_cut_batch(int32_t device, int32_t count, const int32_t* no
       j.sink = sink[g];
       j.m = m[g];
       j.inc_off = dptr<int32_t>(d_blob, off[g][0]);
-      j.inc = dptr<int32_t>(d_blob, off[g][1]);
+      j.ient = dptr<pb::IEnt>(d_blob, off[g][1]);
+      j.epos = dptr<int2>(d_blob, off[g][7]);
+      j.ret_pt = rets[g].a;
+      j.ret_ph = rets[g].b;
       j.tail = dptr<int32_t>(d_blob, off[g][2]);
       j.head = dptr<int32_t>(d_blob, off[g][3]);
       j.lower = dptr<int64_t>(d_blob, off[g][4]);

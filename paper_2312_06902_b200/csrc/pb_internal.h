@@ -1,8 +1,19 @@
 // Internal layout shared by the host packer (pb_host.cpp) and the sm_100a
 // kernels (pb_kernels.cu).  Not part of the public ABI.
+//
+// Design rule: every per-level step of the walk (one BFS level, one
+// longest-path level) must wait on at most ONE dependent global load.  Hence
+//   * computations are renumbered level-major (Kahn depth), so a level is a
+//     contiguous id range and static per-level data can be prefetched;
+//   * the flow network is stored by incidence POSITION: entry p of node x's
+//     list carries {other end, twin position, other's list range}, and the
+//     residual of traversing p away from x lives at resid[p].  A BFS level
+//     therefore loads {ient[p], resid[p]} in parallel and nothing else;
+//   * the visited set and the frontier live in shared memory.
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "perseus_b200.h"
 
@@ -14,34 +25,63 @@ enum : int32_t { kModeDiscover = 0, kModeGetNext = 1 };
 // Internal per-instance status beyond pb_status.
 enum : int32_t { kStatusLogFull = 100 };
 
+// Incidence entry (16 B, one LDG.128): the arc leaving the owning node.
+struct IEnt {
+  int32_t other;      // node at the other end
+  int32_t twin;       // position of the same edge in other's list
+  int32_t other_off;  // other's list = [other_off, other_end)
+  int32_t other_end;
+};
+
+// Host mirrors of the int2 / int4 layouts (no CUDA headers needed).
+struct int2h {
+  int32_t x, y;
+};
+struct int4h {
+  int32_t x, y, z, w;
+};
+
+// Host-built position-indexed incidence (pb_host.cpp build_net).
+struct NetLayout {
+  std::vector<int32_t> inc_off;
+  std::vector<IEnt> ient;
+  std::vector<int2h> epos;
+};
+void build_net(int32_t V, const std::vector<int32_t>& tail, const std::vector<int32_t>& head,
+               NetLayout& out);
+
 // One packed instance: every pointer is a DEVICE address into the batch blob
-// (static data) or the output blob.  Node-DAG ids: computations 0..n-1,
-// virtual source n, sink n+1.  Edge-centric ids (dag.hpp:209-224):
-// computation i -> edge i from node 2i to 2i+1; dependency j -> edge n+j;
-// edge n+ne is the phase-A return arc sink->source (flow.hpp:196-200).
+// (static data) or the output blob.
+//
+// Internal ids: computation i (0..n-1) in level-major order, orig[i] is the
+// caller's id; node-DAG virtual source n, sink n+1.  Edge-centric network
+// (dag.hpp:209-224): computation i -> nodes 2i (start), 2i+1 (end), source
+// 2n, sink 2n+1; edge i = computation edge 2i -> 2i+1, edge n+j = dependency
+// j (caller's order), edge n+ne = phase-A return arc sink -> source
+// (flow.hpp:196-200).
 struct DevInst {
   int32_t n, ne, n_levels, mode;
-  int32_t max_steps, cap_points, cap_ids, pad0;
+  int32_t max_steps, cap_points, V, E;  // E includes the return arc
+  int32_t ret_pt, ret_ph, pad0, pad1;   // return-arc positions (sink side, source side)
   int64_t tau;
   double watts;
   int64_t quantum;
-  // node DAG
+  // node DAG (internal ids)
+  const int32_t* orig;        // [n]
   const int32_t* comp_class;  // [n]
+  const uint8_t* cflag;       // [n] bit 1: has an edge to the sink
   const int32_t* lvl_off;     // [n_levels + 1]
-  const int32_t* lvl_comps;   // [n], topological levels (Kahn depth)
-  const int32_t* in_off;      // [n + 1]
-  const int32_t* in_dep;      // dependency ids j with head == comp
-  const int32_t* out_off;     // [n + 1]
-  const int32_t* out_dep;     // dependency ids j with tail == comp
-  const int32_t* snk_dep;     // dependency ids j with head == sink
-  int32_t n_snk, pad1;
-  const int32_t* dep_tail;  // [ne] node-DAG ids
-  const int32_t* dep_head;  // [ne]
-  // edge-centric incidence (flow network), V = 2n + 2 nodes, E = n + ne + 1
-  const int32_t* inc_off;  // [V + 1]
-  const int32_t* inc;      // (edge << 1) | dir, dir = 1 when the node is the head
-  const int32_t* ec_tail;  // [E]
-  const int32_t* ec_head;  // [E]
+  const int4* frow;           // [n] {count | has-sink << 16, first 3 predecessors}
+  const int4* brow;           // [n] {count, first 3 successors}
+  const int32_t* pin_off;     // [n + 1] computation predecessors
+  const int32_t* pin;
+  const int32_t* pout_off;    // [n + 1] computation successors
+  const int32_t* pout;
+  const int2* dep_nd;         // [ne] node-DAG endpoints (n = source, n + 1 = sink)
+  // edge-centric flow network
+  const int32_t* inc_off;     // [V + 1]
+  const IEnt* ient;           // [2E]
+  const int2* epos;           // [E] {position at tail, position at head}
   // cost model
   const uint8_t* cls_const;   // [classes]
   const int64_t* cls_tmin;    // [classes] curve t_min (table origin)
@@ -52,7 +92,7 @@ struct DevInst {
   const int64_t* pt_energy;
   const double* tables;           // E(t) = a exp(b t) + c for t in [t_min, t_max]
   const double* cls_curve;        // [3 * classes] a, b, c (extrapolation only)
-  const int64_t* start_planned_t; // get-next mode only
+  const int64_t* start_planned_t; // get-next mode only (internal order)
   // outputs; delta records go to the batch-wide pool (DeltaPool)
   pb_point* points;             // [cap_points]
   pb_frontier_summary* summary; // [1]
@@ -61,7 +101,7 @@ struct DevInst {
 // Batch-wide append-only delta log: each step reserves a contiguous range
 // with one atomicAdd, so only the used prefix is copied back.
 struct DeltaPool {
-  int32_t* ids;      // +(c + 1) sped up, -(c + 1) slowed down
+  int32_t* ids;      // +(c + 1) sped up, -(c + 1) slowed down (caller ids)
   uint8_t* choice;   // new Pareto index of that computation
   unsigned long long* cursor;
   long long cap;
@@ -75,15 +115,26 @@ enum : int {
   kPrSlots
 };
 
-// Per-warp workspace slot; arrays sized for the largest instance of a batch.
-// The flow f[] persists across the steps of a walk (warm start).
+// Shared memory per walker warp: visited bitset + ping-pong frontier.
+constexpr int kFrontCap = 64;  // frontier entries per buffer kept in smem
+
+// Per-warp global workspace; arrays sized for the largest instance of a batch.
+// The flow (encoded in resid) persists across the steps of a walk.
 struct WsLayout {
   int64_t max_n, max_v, max_e;
-  int64_t off_lo, off_up, off_f, off_inf, off_crit;      // per edge
-  int64_t off_bal, off_vis, off_par, off_mk;             // per node
-  int64_t off_planned, off_estart, off_lend, off_rstart, off_rdur, off_pdur, off_choice;  // per comp
-  int64_t off_f0, off_f1, off_touch, off_exl, off_delta;  // lists
+  int64_t off_resid;                   // int64 [2E] residual by position
+  int64_t off_bal;                     // int64 [V] phase-A imbalance
+  int64_t off_log;                     // int2  [V] BFS log {position, parent log index}
+  int64_t off_front;                   // int4  [2V] frontier overflow (ping-pong)
+  int64_t off_ecrit;                   // u8    [E] edge critical in the current network
+  int64_t off_durp, off_durr;          // int64 [n]
+  int64_t off_hl;                      // int64x2 [n] {planned duration + tail, 0}
+  int64_t off_fin;                     // int64x2 [n] {finish planned, finish realized}
+  int64_t off_cap;                     // int64x2 [n] {lower, upper (-1 = infinite)}
+  int64_t off_ccrit, off_choice;       // u8 [n]
+  int64_t off_touch, off_exl, off_delta, off_path;  // int32 lists
   int64_t stride;
+  int32_t smem_bytes;  // dynamic shared memory per warp
 };
 
 struct RunCounters {
@@ -107,38 +158,37 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
     o = align_up(o + bytes, 256);
     return at;
   };
-  L.off_lo = take(8 * max_e);
-  L.off_up = take(8 * max_e);
-  L.off_f = take(8 * max_e);
-  L.off_inf = take(max_e);
-  L.off_crit = take(max_e);
+  L.off_resid = take(8 * 2 * max_e);
   L.off_bal = take(8 * max_v);
-  L.off_vis = take(4 * max_v);
-  L.off_par = take(4 * max_v);
-  L.off_mk = take(4 * max_v);
-  L.off_planned = take(8 * max_n);
-  L.off_estart = take(8 * max_n);
-  L.off_lend = take(8 * max_n);
-  L.off_rstart = take(8 * max_n);
-  L.off_rdur = take(8 * max_n);
-  L.off_pdur = take(8 * max_n);
+  L.off_log = take(8 * max_v);
+  L.off_front = take(16 * 2 * max_v);
+  L.off_ecrit = take(max_e);
+  L.off_durp = take(8 * max_n);
+  L.off_durr = take(8 * max_n);
+  L.off_hl = take(16 * max_n);
+  L.off_fin = take(16 * max_n);
+  L.off_cap = take(16 * max_n);
+  L.off_ccrit = take(max_n);
   L.off_choice = take(max_n);
-  L.off_f0 = take(4 * max_v);
-  L.off_f1 = take(4 * max_v);
   L.off_touch = take(4 * 2 * max_e);
   L.off_exl = take(4 * max_v);
   L.off_delta = take(4 * max_n);
+  L.off_path = take(4 * max_v);
   L.stride = o;
+  const int64_t bitwords = (max_v + 31) / 32;
+  L.smem_bytes = static_cast<int32_t>(align_up(4 * bitwords, 16) + 16 * 2 * kFrontCap);
   return L;
 }
 
-// Generic flow-graph job for pb_flow_min_cut_batch: the same push-relabel
-// device code on an arbitrary FlowGraph (flow.hpp:22-80).
+// Generic flow-graph job for pb_flow_min_cut_batch: the same device max-flow
+// code on an arbitrary FlowGraph (flow.hpp:22-80).  Edge m = return arc.
 struct DevFlowJob {
   int32_t nodes, source, sink, m;
+  int32_t ret_pt, ret_ph, pad0, pad1;
   const int32_t* inc_off;  // [nodes + 1]
-  const int32_t* inc;      // (edge << 1) | dir
-  const int32_t* tail;     // [m + 1], edge m = return arc sink -> source
+  const IEnt* ient;        // [2(m + 1)]
+  const int2* epos;        // [m + 1]
+  const int32_t* tail;     // [m]
   const int32_t* head;
   const int64_t* lower;    // [m]
   const int64_t* upper;    // [m]
@@ -153,21 +203,22 @@ struct DevFlowJob {
   int8_t* cut_dir; // [m]
 };
 
-// Host-side launchers (pb_kernels.cu).
-// slots = number of walker warps (one workspace each).
-int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
-                 char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
-                 DeltaPool pool, void* stream);
-int walk_slots_per_sm();
-int launch_flow_jobs(const DevFlowJob* d_jobs, int32_t count, char* d_ws, const WsLayout& ws,
-                     int32_t slots, void* stream);
-// annotate_slack job outputs (per DAG).
+// annotate_slack job outputs (per DAG, caller ids).
 struct SlackOut {
-  const int64_t* dur;
+  const int64_t* dur;  // [n] caller order
   int64_t* earliest;
   int64_t* latest;
   uint8_t* critical;
 };
+
+// Host-side launchers (pb_kernels.cu).  slots = number of walker warps (one
+// workspace each).
+int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
+                 char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
+                 DeltaPool pool, void* stream);
+int walk_slots_per_sm(const WsLayout& ws);
+int launch_flow_jobs(const DevFlowJob* d_jobs, int32_t count, char* d_ws, const WsLayout& ws,
+                     int32_t slots, void* stream);
 int launch_slack_jobs(const DevInst* d_insts, const SlackOut* d_outs, int64_t* d_makespan,
                       int32_t count, char* d_ws, const WsLayout& ws, int32_t slots, void* stream);
 

@@ -1,31 +1,33 @@
-// sm_100a kernels of the B200-native Perseus frontier generator.
+// sm_100a kernels of the B200-native Perseus frontier generator (v4).
 //
 // One WARP walks one instance's whole frontier (frontier.hpp:166-189) inside
 // a single persistent launch: warps pull instances (LPT order) from a global
 // counter, so thousands of walks are in flight and no host round trip
-// happens per step.  All synchronization is __syncwarp, appends are ballot
-// compactions, deduplication is __match_any_sync + a stamp.  Per step:
+// happens per step.  Synchronization is __syncwarp only; appends are ballot
+// compactions.  Per step:
 //
-//   K2  longest path over static node-DAG levels (annotate_slack,
-//       dag.hpp:233-286; simulate, emulator.hpp:28-55): pull-based,
-//       deterministic;
+//   K2  ONE fused longest-path sweep over the level-major computation order:
+//       lanes 0-15 run the forward pass (planned AND realized finish times,
+//       simulate, emulator.hpp:28-55; earliest, dag.hpp:266-271), lanes 16-31
+//       the backward pass (tail lengths; latest = makespan - tail,
+//       dag.hpp:272-277).  Static per-level data is software-pipelined one
+//       level ahead, so a level waits on one dependent load;
 //   K3  fused critical mask + Eq. 7 capacities (build_capacity_dag,
 //       flow.hpp:285-317) from host-tabulated curve values, with the
-//       reference's int128 overflow checks (flow.hpp:58-68, 196-197);
-//   K4  max flow with lower bounds, WARM-STARTED: the flow of the previous
-//       step is kept, clamped into the new bounds (edges leaving the critical
-//       sub-DAG drop to 0, new ones start at their lower bound), and the
-//       resulting node imbalances are repaired by multi-source BFS
-//       augmentation in the circulation network with the return arc
-//       sink->source (phase A = the feasibility test of flow.hpp:172-203);
-//       phase B then augments source->sink along BFS-shortest residual
-//       paths (flow.hpp:205-228).  Steps change few capacities, so a step
-//       needs ~1-4 BFS instead of a from-scratch max flow;
-//   K5  the last phase-B BFS (sink unreachable) visits exactly the source
+//       reference's int128 overflow checks (flow.hpp:58-68, 196-197).  Flows
+//       persist across steps (warm start) and are clamped into the new
+//       bounds; infinite edges store -(f + 1) so the sentinel can change
+//       without touching them;
+//   K4  max flow with lower bounds: the clamp imbalances are repaired by
+//       multi-source BFS augmentation in the circulation network with the
+//       return arc sink->source (phase A = the feasibility test of
+//       flow.hpp:172-203), then source->sink BFS augmentation (phase B,
+//       flow.hpp:205-228).  A BFS level loads {ient[p], resid[p]} for its
+//       arcs in parallel; the visited set is a shared-memory bitset;
+//   K5  the last phase-B BFS (sink unreachable) marks exactly the source
 //       side of the minimal minimum cut (min_cut_from_flow, flow.hpp:234-262);
 //       tau update with the reference's skip rules (frontier.hpp:111-131),
-//       discretize (frontier.hpp:140-161), realized longest path,
-//       append-only delta log.
+//       discretize (frontier.hpp:140-161), append-only delta log.
 //
 // Only the unique minimal min cut and the two verdicts (feasible, value >=
 // sentinel) feed the outputs, so the flow itself is free to differ from the
@@ -87,162 +89,182 @@ __device__ __forceinline__ void wappend(bool pred, int val, int32_t* list, int& 
   count += __popc(m);
 }
 
-__device__ __forceinline__ void red_add(int64_t* p, long long d) {
+__device__ __forceinline__ void red_add(long long* p, long long d) {
   atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(d));
 }
 
+__device__ __forceinline__ long long now() { return clock64(); }
+
+// Work counters: per-lane in registers (flushed once per warp), phase
+// profile in shared memory (lane 0 only).
 struct Counters {
-  unsigned long long arc_scans = 0, node_updates = 0, rounds = 0, comp_visits = 0;
-  unsigned long long prof[kPrSlots] = {};
+  unsigned arc_scans = 0, node_updates = 0, comp_visits = 0;
+  unsigned long long* prof = nullptr;
   __device__ void add(int slot, long long v) {
     if (lane_id() == 0) prof[slot] += static_cast<unsigned long long>(v);
   }
 };
 
-__device__ __forceinline__ long long now() { return clock64(); }
+// Effective residual of a raw position value: >= 0 is a plain residual;
+// < 0 encodes the forward side of an infinite edge carrying f = -raw - 1,
+// whose residual is sentinel - f.  Augmentation arithmetic (raw -= d,
+// twin += d) is the same for both encodings.
+__device__ __forceinline__ long long eff_res(long long raw, long long S) {
+  return raw >= 0 ? raw : S + 1 + raw;
+}
 
-// Flow-network view of one warp's workspace.  Edge ids: graph edges, then the
-// return arc `ret` (sink -> source, capacity kHuge, enabled in phase A only);
-// f[ret] is the circulation's s->t value R.
+// Flow-network view of one warp's workspace.
 struct Net {
-  int V, E, src, snk, ret;
+  int V, src, snk, ret_pt, ret_ph, nbitw, fstride;
   const int32_t* inc_off;
-  const int32_t* inc;  // (edge << 1) | dir, dir = 1 when the node is the head
-  const int32_t* tail;
-  const int32_t* head;
-  int64_t* lo;
-  int64_t* up;  // finite upper bound (ignored when inf)
-  int64_t* f;   // absolute flow, persistent across steps
-  uint8_t* inf;
-  uint8_t* crit;  // edge present in the current network
-  int64_t* bal;   // inflow - outflow (phase-A imbalance)
-  int32_t* vis;   // BFS stamp
-  int32_t* par;   // BFS parent code (edge << 1) | backward
-  int32_t* mk;    // list dedup stamp
-  int32_t* f0;
-  int32_t* f1;
+  const IEnt* ient;
+  long long* resid;
+  long long* bal;
+  int2* lg;        // BFS log: {position used to reach the node, parent log index}
+  int4* fglob;     // frontier overflow, 2 buffers of fstride entries
+  uint32_t* bits;  // smem visited bitset
+  int4* fs;        // smem frontier, 2 buffers of kFrontCap entries
+  int32_t* path;
   int32_t* touch;
   int32_t* exl;
-  long long sentinel;
-  int stamp, mstamp;
-  bool ret_on;
+  long long S;  // infinity sentinel of the current network
+  long long R;  // flow on the return arc = s->t value
 };
 
-__device__ __forceinline__ long long upres(const Net& N, int ed) {
-  return ed == N.ret ? kHuge : (N.inf[ed] ? N.sentinel : N.up[ed]);
-}
-// Residual capacity of traversing incidence entry a away from its node:
-// forward (node is tail) = upper - f, backward (node is head) = f - lower.
-__device__ __forceinline__ long long residual_from(const Net& N, int a) {
-  const int ed = a >> 1;
-  if (ed == N.ret ? !N.ret_on : !N.crit[ed]) return 0;
-  return (a & 1) ? N.f[ed] - N.lo[ed] : upres(N, ed) - N.f[ed];
-}
-__device__ __forceinline__ int other_end(const Net& N, int a) {
-  const int ed = a >> 1;
-  return (a & 1) ? N.tail[ed] : N.head[ed];
+__device__ __forceinline__ int4* fslot(const Net& N, int buf, int k) {
+  return k < kFrontCap ? &N.fs[buf * kFrontCap + k] : &N.fglob[static_cast<size_t>(buf) * N.fstride + k];
 }
 
-// Level-synchronous BFS over residual arcs from `nsrc` sources in N.f0.
-// phaseA: targets are nodes with bal < 0; phaseB: the sink.  Stops at the
-// first level that reaches a target and returns it (-1: none reachable; then
-// the stamp N.stamp marks exactly the residual-reachable set).
-__device__ int bfs(Net& N, int nsrc, bool phaseA, Counters& C) {
+__device__ __forceinline__ void clear_bits(Net& N) {
+  for (int w = lane_id(); w < N.nbitw; w += 32) N.bits[w] = 0;
+  __syncwarp();
+}
+// true when this call set the bit
+__device__ __forceinline__ bool test_and_set(Net& N, int u) {
+  const uint32_t m = 1u << (u & 31);
+  return (atomicOr(&N.bits[u >> 5], m) & m) == 0;
+}
+__device__ __forceinline__ bool bit_of(const Net& N, int u) { return (N.bits[u >> 5] >> (u & 31)) & 1u; }
+
+// Seeds frontier slot k (buffer 0) and log entry k with node v.
+__device__ __forceinline__ void seed(Net& N, int k, int v) {
+  *fslot(N, 0, k) = make_int4(v, N.inc_off[v], N.inc_off[v + 1], k);
+  N.lg[k] = make_int2(-1 - v, -1);
+}
+
+// Level-synchronous BFS over residual arcs from the nsrc seeded sources
+// (already marked).  phaseA: targets are nodes with bal < 0; phase B: the
+// sink.  Stops after the level that reaches a target and returns its log
+// index (tgt = node); -1 when none is reachable, and then the bitset marks
+// exactly the residual-reachable set.
+__device__ int bfs(Net& N, int nsrc, bool phaseA, int& tgt, Counters& C) {
   const int ln = lane_id();
   const long long t0 = now();
-  ++N.stamp;
-  const int stamp = N.stamp;
-  for (int i = ln; i < nsrc; i += 32) {
-    const int v = N.f0[i];
-    N.vis[v] = stamp;
-    N.par[v] = -1;
-  }
-  __syncwarp();
-  int cnt = nsrc;
-  int32_t* F = N.f0;
-  int32_t* G = N.f1;
-  int found = -1;
+  int cnt = nsrc, cur = 0, nlog = nsrc, found = -1;
+  tgt = -1;
   while (cnt > 0 && found < 0) {
     C.add(kPrBfsLevels, 1);
+    const int lg2 = cnt >= 16 ? 0 : cnt >= 8 ? 1 : cnt >= 4 ? 2 : 3;  // lanes per frontier node
+    const int g = 1 << lg2;
+    const int sub = ln & (g - 1);
     int nc = 0;
-    for (int base = 0; base < cnt; base += 32) {
-      const int i = base + ln;
-      const bool valid = i < cnt;
-      const int w = valid ? F[i] : 0;
-      const int off = valid ? N.inc_off[w] : 0;
-      const int deg = valid ? N.inc_off[w + 1] - off : 0;
-      const int md = wmaxi(deg);
-      if (valid) C.arc_scans += deg;
-      for (int j = 0; j < md; ++j) {
+    for (int base = 0; base < cnt; base += 32 >> lg2) {
+      const int slot = base + (ln >> lg2);
+      const bool valid = slot < cnt;
+      int4 fe = make_int4(0, 0, 0, 0);
+      if (valid) fe = *fslot(N, cur, slot);
+      const int deg = fe.z - fe.y;
+      const int myr = deg > sub ? (deg - sub + g - 1) >> lg2 : 0;
+      const int rounds = wmaxi(myr);
+      C.arc_scans += myr;
+      for (int r = 0; r < rounds; ++r) {
+        const int p = fe.y + sub + (r << lg2);
         bool cand = false;
-        int u = 0, a = 0;
-        if (j < deg) {
-          a = N.inc[off + j];
-          if (residual_from(N, a) > 0) {
-            u = other_end(N, a);
-            cand = N.vis[u] != stamp;
+        IEnt e{0, 0, 0, 0};
+        if (r < myr) {
+          e = N.ient[p];
+          const long long raw = N.resid[p];
+          if (eff_res(raw, N.S) > 0) cand = test_and_set(N, e.other);
+        }
+        const unsigned m = __ballot_sync(kFull, cand);
+        if (m) {
+          const int pos = nc + __popc(m & lanemask_lt());
+          bool hit = false;
+          if (cand) {
+            const int li = nlog + pos;
+            N.lg[li] = make_int2(p, fe.w);
+            *fslot(N, cur ^ 1, pos) = make_int4(e.other, e.other_off, e.other_end, li);
+            hit = phaseA ? N.bal[e.other] < 0 : e.other == N.snk;
+            ++C.node_updates;
           }
+          const unsigned h = __ballot_sync(kFull, hit);
+          if (h && found < 0) {
+            const int hl = __ffs(h) - 1;
+            found = __shfl_sync(kFull, nlog + pos, hl);
+            tgt = __shfl_sync(kFull, e.other, hl);
+          }
+          nc += __popc(m);
         }
-        const unsigned peers = __match_any_sync(kFull, cand ? u : -1 - ln);
-        const bool lead = cand && (__ffs(peers) - 1) == ln;
-        bool hit = false;
-        if (lead) {
-          N.vis[u] = stamp;
-          N.par[u] = ((a >> 1) << 1) | (a & 1);
-          ++C.node_updates;
-          hit = phaseA ? N.bal[u] < 0 : u == N.snk;
-        }
-        const unsigned h = __ballot_sync(kFull, hit);
-        if (h && found < 0) found = __shfl_sync(kFull, u, __ffs(h) - 1);
-        wappend(lead, u, G, nc);
-        __syncwarp();
       }
     }
+    __syncwarp();
+    nlog += nc;
     cnt = nc;
-    int32_t* t = F;
-    F = G;
-    G = t;
+    cur ^= 1;
   }
   __syncwarp();
   C.add(kPrBfs, now() - t0);
   return found;
 }
 
-// Augments along the BFS parent chain ending at `tgt` (lane 0; the path is a
-// pointer chase).  Phase A: amount = min(residuals, bal[src], -bal[tgt]) and
-// the balances move; phase B: amount = min(residuals) and R grows.
-__device__ void augment(Net& N, int tgt, bool phaseA, Counters& C) {
+// Augments along the logged BFS path ending at log index `found` (node tgt):
+// lane 0 chases the parent links (one load per hop), then the warp updates
+// both sides of every path arc.  Phase A: amount = min(residuals, bal[src],
+// -bal[tgt]) and the balances move; phase B: amount = min(residuals), R grows.
+__device__ void augment(Net& N, int found, int tgt, bool phaseA, Counters& C) {
+  const int ln = lane_id();
   const long long t0 = now();
-  if (lane_id() == 0) {
-    long long d = phaseA ? -N.bal[tgt] : LLONG_MAX;
-    int v = tgt, hops = 0;
-    while (N.par[v] != -1) {
-      const int code = N.par[v];
-      const int ed = code >> 1;
-      const long long r = (code & 1) ? N.f[ed] - N.lo[ed] : upres(N, ed) - N.f[ed];
+  long long d = 0;
+  int k = 0, src = -1;
+  if (ln == 0) {
+    d = phaseA ? -N.bal[tgt] : LLONG_MAX;
+    int idx = found;
+    for (;;) {
+      const int2 l = N.lg[idx];
+      if (l.x < 0) {
+        src = -1 - l.x;
+        break;
+      }
+      const long long r = eff_res(N.resid[l.x], N.S);
       d = r < d ? r : d;
-      v = (code & 1) ? N.head[ed] : N.tail[ed];
-      ++hops;
-    }
-    if (phaseA) d = N.bal[v] < d ? N.bal[v] : d;
-    const int src = v;
-    v = tgt;
-    while (N.par[v] != -1) {
-      const int code = N.par[v];
-      const int ed = code >> 1;
-      N.f[ed] += (code & 1) ? -d : d;
-      v = (code & 1) ? N.head[ed] : N.tail[ed];
+      N.path[k++] = l.x;
+      idx = l.y;
     }
     if (phaseA) {
+      const long long b = N.bal[src];
+      d = b < d ? b : d;
+    }
+  }
+  d = __shfl_sync(kFull, d, 0);
+  k = __shfl_sync(kFull, k, 0);
+  src = __shfl_sync(kFull, src, 0);
+  __syncwarp();
+  for (int q = ln; q < k; q += 32) {
+    const int p = N.path[q];
+    N.resid[p] -= d;
+    N.resid[N.ient[p].twin] += d;
+  }
+  if (phaseA) {
+    if (ln == 0) {
       N.bal[src] -= d;
       N.bal[tgt] += d;
-    } else {
-      N.f[N.ret] += d;
     }
-    C.prof[kPrPaths] += 1;
-    C.prof[kPrPathHops] += hops;
-    C.node_updates += 2 * hops;
+  } else {
+    N.R += d;
   }
+  C.add(kPrPaths, 1);
+  C.add(kPrPathHops, k);
+  if (ln == 0) C.node_updates += 2 * k;
   __syncwarp();
   C.add(kPrAugment, now() - t0);
 }
@@ -253,145 +275,203 @@ __device__ void augment(Net& N, int tgt, bool phaseA, Counters& C) {
 // network is infeasible (max_flow_lower_bounds returns nullopt).
 __device__ bool repair(Net& N, int ntouch, Counters& C) {
   const int ln = lane_id();
-  // distinct touched nodes with excess
-  ++N.mstamp;
+  clear_bits(N);
   int nex = 0;
   for (int base = 0; base < ntouch; base += 32) {
     const int i = base + ln;
-    const bool valid = i < ntouch;
-    const int v = valid ? N.touch[i] : 0;
-    const unsigned peers = __match_any_sync(kFull, valid ? v : -1 - ln);
-    bool take = valid && (__ffs(peers) - 1) == ln && N.mk[v] != N.mstamp;
-    if (take) N.mk[v] = N.mstamp;
-    take = take && N.bal[v] > 0;
+    bool take = false;
+    int v = 0;
+    if (i < ntouch) {
+      v = N.touch[i];
+      take = test_and_set(N, v) && N.bal[v] > 0;
+    }
     wappend(take, v, N.exl, nex);
-    __syncwarp();
   }
+  __syncwarp();
   if (nex == 0) return true;
   C.add(kPrImbalanced, nex);
   const long long t0 = now();
-  N.ret_on = true;
+  if (ln == 0) {
+    N.resid[N.ret_pt] = kHuge - N.R;
+    N.resid[N.ret_ph] = N.R;
+  }
+  __syncwarp();
   bool ok = true;
   for (;;) {
+    clear_bits(N);
     int ns = 0;
     for (int base = 0; base < nex; base += 32) {
       const int i = base + ln;
       const int v = i < nex ? N.exl[i] : 0;
-      wappend(i < nex && N.bal[v] > 0, v, N.f0, ns);
+      const bool pred = i < nex && N.bal[v] > 0;
+      const unsigned m = __ballot_sync(kFull, pred);
+      if (pred) {
+        const int k = ns + __popc(m & lanemask_lt());
+        N.exl[k] = v;
+        test_and_set(N, v);
+        seed(N, k, v);
+      }
+      ns += __popc(m);
     }
     __syncwarp();
     if (ns == 0) break;
-    for (int i = ln; i < ns; i += 32) N.exl[i] = N.f0[i];
     nex = ns;
-    __syncwarp();
     C.add(kPrBfsA, 1);
-    const int tgt = bfs(N, ns, true, C);
-    if (tgt < 0) {
+    int tgt;
+    const int found = bfs(N, ns, true, tgt, C);
+    if (found < 0) {
       ok = false;
       break;
     }
-    augment(N, tgt, true, C);
+    augment(N, found, tgt, true, C);
   }
-  N.ret_on = false;
+  __syncwarp();
+  N.R = N.resid[N.ret_ph];
+  __syncwarp();
+  if (ln == 0) {
+    N.resid[N.ret_pt] = 0;
+    N.resid[N.ret_ph] = 0;
+  }
+  __syncwarp();
   C.add(kPrPhaseA, now() - t0);
   return ok;
 }
 
 // Phase B: source->sink augmentation until the sink is unreachable; the
-// last BFS stamp then marks the minimal min cut's source side.
+// bitset then marks the minimal min cut's source side.
 __device__ void maximize(Net& N, Counters& C) {
   const long long t0 = now();
   for (;;) {
-    if (lane_id() == 0) N.f0[0] = N.src;
+    clear_bits(N);
+    if (lane_id() == 0) {
+      test_and_set(N, N.src);
+      seed(N, 0, N.src);
+    }
     __syncwarp();
     C.add(kPrBfsB, 1);
-    const int tgt = bfs(N, 1, false, C);
-    if (tgt < 0) break;
-    augment(N, tgt, false, C);
+    int tgt;
+    const int found = bfs(N, 1, false, tgt, C);
+    if (found < 0) break;
+    augment(N, found, tgt, false, C);
   }
   C.add(kPrPhaseB, now() - t0);
-}
-
-// Records a flow change on edge ed: imbalance at both ends, both touched.
-__device__ __forceinline__ void flow_change(Net& N, int ed, long long delta) {
-  red_add(&N.bal[N.head[ed]], delta);
-  red_add(&N.bal[N.tail[ed]], -delta);
 }
 
 // ------------------------------------------------------------------ walk
 
 struct Walk {
-  int64_t* planned;
-  int64_t* estart;
-  int64_t* lend;
-  int64_t* rstart;
-  int64_t* rdur;
-  int64_t* pdur;
+  long long* durp;   // planned durations
+  long long* durr;   // realized (discretized) durations
+  longlong2* fin;    // {planned finish, realized finish}
+  longlong2* tl;     // {planned duration + longest tail to the sink, 0}
+  longlong2* cap;    // {lower, upper; -1 = infinite} of critical computation edges
+  uint8_t* ecrit;    // [E] edge in the current critical network
   uint8_t* choice;
   int32_t* delta;
 };
 
-// Level-synchronous longest path on the node DAG (simulate,
-// emulator.hpp:28-55; forward half of annotate_slack, dag.hpp:266-271).
-// start[i] = max over predecessors (start[u] + dur[u]); returns makespan.
-__device__ long long forward_pass(const DevInst& I, const int64_t* dur, int64_t* start, Counters& C) {
+// Fused longest path over the level-major order (K2).  Forward lanes (0-15)
+// compute fin[i] = max over predecessors of fin + (dp[i], dr[i]); backward
+// lanes (16-31, when `back`) compute tl[i].x = dp[i] + max over successors
+// tl.x.  Level k of the forward pass and level L-1-k of the backward pass run
+// in the same iteration.  The per-level static data (row records, level
+// bounds) and the durations are loaded one iteration ahead.
+__device__ void sweep(const DevInst& I, const long long* dp, const long long* dr, longlong2* fin,
+                      longlong2* tl, bool back, long long& msp, long long& msr, Counters& C) {
   const int ln = lane_id();
   const long long t0 = now();
-  C.add(kPrLpLevels, I.n_levels);
-  for (int L = 0; L < I.n_levels; ++L) {
-    const int b = I.lvl_off[L], e = I.lvl_off[L + 1];
-    for (int q = b + ln; q < e; q += 32) {
-      const int i = I.lvl_comps[q];
-      long long m = 0;
-      for (int j = I.in_off[i]; j < I.in_off[i + 1]; ++j) {
-        const int u = I.dep_tail[I.in_dep[j]];
-        if (u < I.n) {
-          const long long c = start[u] + dur[u];
-          if (c > m) m = c;
+  const bool fwd = ln < 16;
+  const int s = ln & 15;
+  const int L = I.n_levels;
+  const bool active = fwd || back;
+  const int4* row = fwd ? I.frow : I.brow;
+  const int32_t* noff = fwd ? I.pin_off : I.pout_off;
+  const int32_t* nb = fwd ? I.pin : I.pout;
+  longlong2* vals = fwd ? fin : tl;
+  long long mp = 0, mr = 0;
+  C.add(kPrLpLevels, L);
+  auto lev_of = [&](int k) { return fwd ? k : L - 1 - k; };
+  int b0 = 0, e0 = 0, b1 = 0, e1 = 0;
+  if (active && L > 0) {
+    b0 = I.lvl_off[lev_of(0)];
+    e0 = I.lvl_off[lev_of(0) + 1];
+  }
+  if (active && L > 1) {
+    b1 = I.lvl_off[lev_of(1)];
+    e1 = I.lvl_off[lev_of(1) + 1];
+  }
+  int4 r0 = make_int4(0, 0, 0, 0);
+  long long dp0 = 0, dr0 = 0;
+  if (b0 + s < e0) {
+    r0 = row[b0 + s];
+    dp0 = dp[b0 + s];
+    dr0 = fwd ? dr[b0 + s] : 0;
+  }
+  for (int k = 0; k < L; ++k) {
+    // issue the loads of the next iterations
+    int b2 = 0, e2 = 0;
+    if (active && k + 2 < L) {
+      b2 = I.lvl_off[lev_of(k + 2)];
+      e2 = I.lvl_off[lev_of(k + 2) + 1];
+    }
+    int4 r1 = make_int4(0, 0, 0, 0);
+    long long dp1 = 0, dr1 = 0;
+    if (b1 + s < e1) {
+      r1 = row[b1 + s];
+      dp1 = dp[b1 + s];
+      dr1 = fwd ? dr[b1 + s] : 0;
+    }
+    const int i0 = b0 + s;
+    if (i0 < e0) {
+      const int cnt = r0.x & 0xffff;
+      long long x = 0, y = 0;
+      longlong2 v0 = make_longlong2(0, 0), v1 = v0, v2 = v0;
+      if (cnt > 0) v0 = vals[r0.y];
+      if (cnt > 1) v1 = vals[r0.z];
+      if (cnt > 2) v2 = vals[r0.w];
+      x = max(max(v0.x, v1.x), max(v2.x, x));
+      y = max(max(v0.y, v1.y), max(v2.y, y));
+      if (cnt > 3)
+        for (int j = noff[i0] + 3; j < noff[i0 + 1]; ++j) {
+          const longlong2 v = vals[nb[j]];
+          x = max(x, v.x);
+          y = max(y, v.y);
         }
+      const long long a = x + dp0, c = fwd ? y + dr0 : 0;
+      vals[i0] = make_longlong2(a, c);
+      if (fwd && (r0.x >> 16)) {
+        mp = max(mp, a);
+        mr = max(mr, c);
       }
-      start[i] = m;
       ++C.comp_visits;
+      // levels wider than 16: the remaining computations, plain CSR
+      for (int i = i0 + 16; i < e0; i += 16) {
+        long long xx = 0, yy = 0;
+        for (int j = noff[i]; j < noff[i + 1]; ++j) {
+          const longlong2 v = vals[nb[j]];
+          xx = max(xx, v.x);
+          yy = max(yy, v.y);
+        }
+        const long long aa = xx + dp[i], cc = fwd ? yy + dr[i] : 0;
+        vals[i] = make_longlong2(aa, cc);
+        if (fwd && (row[i].x >> 16)) {
+          mp = max(mp, aa);
+          mr = max(mr, cc);
+        }
+        ++C.comp_visits;
+      }
     }
     __syncwarp();
+    b0 = b1;
+    e0 = e1;
+    b1 = b2;
+    e1 = e2;
+    r0 = r1;
+    dp0 = dp1;
+    dr0 = dr1;
   }
-  long long ms = 0;
-  for (int q = ln; q < I.n_snk; q += 32) {
-    const int u = I.dep_tail[I.snk_dep[q]];
-    if (u < I.n) {
-      const long long c = start[u] + dur[u];
-      if (c > ms) ms = c;
-    }
-  }
-  ms = wmax(ms);
-  C.add(kPrLp, now() - t0);
-  return ms;
-}
-
-// Backward half of annotate_slack (dag.hpp:272-277): lend[i] = latest time
-// of node 2i+1 = min over successors (lend[v] - dur[v]), makespan at the sink.
-__device__ void backward_pass(const DevInst& I, const int64_t* dur, int64_t* lend, long long ms,
-                              Counters& C) {
-  const int ln = lane_id();
-  const long long t0 = now();
-  C.add(kPrLpLevels, I.n_levels);
-  for (int L = I.n_levels - 1; L >= 0; --L) {
-    const int b = I.lvl_off[L], e = I.lvl_off[L + 1];
-    for (int q = b + ln; q < e; q += 32) {
-      const int i = I.lvl_comps[q];
-      long long m = ms;
-      for (int j = I.out_off[i]; j < I.out_off[i + 1]; ++j) {
-        const int v = I.dep_head[I.out_dep[j]];
-        if (v < I.n) {
-          const long long c = lend[v] - dur[v];
-          if (c < m) m = c;
-        }
-      }
-      lend[i] = m;
-      ++C.comp_visits;
-    }
-    __syncwarp();
-  }
+  msp = wmax(mp);
+  msr = wmax(mr);
   C.add(kPrLp, now() - t0);
 }
 
@@ -439,61 +519,191 @@ __device__ void write_point(const DevInst& I, int k, long long tp, long long tr,
   I.points[k] = p;
 }
 
-__device__ void reset_net(Net& N) {
-  const int ln = lane_id();
-  for (int e = ln; e < N.E; e += 32) {
-    N.f[e] = 0;
-    N.lo[e] = 0;
-    N.up[e] = 0;
-    N.inf[e] = 0;
-    N.crit[e] = 0;
-  }
-  for (int v = ln; v < N.V; v += 32) {
-    N.bal[v] = 0;
-    N.vis[v] = 0;
-    N.mk[v] = 0;
-  }
-  N.stamp = 0;
-  N.mstamp = 0;
-  N.ret_on = false;
-  N.sentinel = 0;
-  __syncwarp();
-}
+__device__ __forceinline__ int ec_tail_of(int n, int u) { return u == n ? 2 * n : 2 * u + 1; }
+__device__ __forceinline__ int ec_head_of(int n, int v) { return v == n + 1 ? 2 * n + 1 : 2 * v; }
 
-// Clamps every infinite critical edge's flow to the new sentinel (only
-// needed when the sentinel shrank below a carried flow; checked by caller).
-__device__ void clamp_infinite(Net& N, int nedges, int& ntouch) {
+// K3: critical mask + Eq. 7 capacities + warm-start clamp for every edge.
+// Returns PB_OK or PB_ERR_OVERFLOW; ntouch = nodes whose balance moved.
+__device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, long long ms, int& ntouch,
+                          int* extrap, Counters& C) {
   const int ln = lane_id();
-  for (int base = 0; base < nedges; base += 32) {
-    const int k = base + ln;
+  const int n = I.n;
+  const long long t0 = now();
+  C.add(kPrSteps, 1);
+  i128 suml = 0, sumu = 0;
+  long long ninf = 0, max_inf_f = 0;
+  ntouch = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + ln;
     bool ch = false;
-    if (k < nedges && N.crit[k] && N.inf[k] && N.f[k] > N.sentinel) {
-      flow_change(N, k, N.sentinel - N.f[k]);
-      N.f[k] = N.sentinel;
-      ch = true;
+    if (i < n) {
+      const int c = I.comp_class[i];
+      const long long t = W.durp[i];
+      const bool crit = W.fin[i].x + W.tl[i].x - t == ms;
+      const bool oc = W.ecrit[i];
+      const int2 ps = I.epos[i];
+      long long fo = 0;
+      if (oc) fo = W.cap[i].x + N.resid[ps.y];
+      long long l = 0, u = 0;
+      bool inf = true;
+      if (crit && !I.cls_const[c]) {
+        const long long tmin = I.cls_tmin[c], tmax = I.cls_tmax[c];
+        const bool can_speed = t - step >= tmin;
+        const bool can_slow = t + step <= tmax;
+        const double et = (can_speed || can_slow) ? table_at(I, c, t, extrap) : 0.0;
+        if (can_slow) {
+          const long long r = llround(et - table_at(I, c, t + step, extrap));
+          l = r > 0 ? r : 0;
+        }
+        if (can_speed) {
+          const long long r = llround(table_at(I, c, t - step, extrap) - et);
+          u = r > l ? r : l;
+          inf = false;
+        }
+      }
+      long long fn = 0;
+      if (crit) {
+        fn = fo < l ? l : fo;
+        if (!inf && fn > u) fn = u;
+        suml += l;
+        if (!inf) {
+          sumu += u;
+        } else {
+          ++ninf;
+          max_inf_f = fn > max_inf_f ? fn : max_inf_f;
+        }
+      }
+      if (crit || oc) {
+        N.resid[ps.x] = crit ? (inf ? -(fn + 1) : u - fn) : 0;
+        N.resid[ps.y] = crit ? fn - l : 0;
+        W.cap[i] = make_longlong2(l, inf ? -1 : u);
+        W.ecrit[i] = crit;
+      }
+      if (fn != fo) {
+        red_add(&N.bal[2 * i + 1], fn - fo);
+        red_add(&N.bal[2 * i], fo - fn);
+        ch = true;
+      }
     }
-    wappend(ch, ch ? N.tail[k] : 0, N.touch, ntouch);
-    wappend(ch, ch ? N.head[k] : 0, N.touch, ntouch);
+    wappend(ch, 2 * i, N.touch, ntouch);
+    wappend(ch, 2 * i + 1, N.touch, ntouch);
   }
   __syncwarp();
+  for (int base = 0; base < I.ne; base += 32) {
+    const int j = base + ln;
+    bool ch = false;
+    int et = 0, eh = 0;
+    if (j < I.ne) {
+      const int2 uv = I.dep_nd[j];
+      const int k = n + j;
+      bool tc = true, hc = true;
+      long long te = 0, he = ms;
+      if (uv.x != n) {
+        tc = W.ecrit[uv.x];
+        te = W.fin[uv.x].x;
+      }
+      if (uv.y != n + 1) {
+        hc = W.ecrit[uv.y];
+        he = W.fin[uv.y].x - W.durp[uv.y];
+      }
+      const bool crit = tc && hc && te == he;
+      const bool oc = W.ecrit[k];
+      const int2 ps = I.epos[k];
+      long long fo = 0;
+      if (oc) fo = N.resid[ps.y];
+      const long long fn = crit ? fo : 0;
+      if (crit || oc) {
+        N.resid[ps.y] = fn;
+        N.resid[ps.x] = crit ? -(fn + 1) : 0;
+        W.ecrit[k] = crit;
+      }
+      if (crit) {
+        ++ninf;
+        max_inf_f = fn > max_inf_f ? fn : max_inf_f;
+      }
+      if (fn != fo) {
+        et = ec_tail_of(n, uv.x);
+        eh = ec_head_of(n, uv.y);
+        red_add(&N.bal[eh], fn - fo);
+        red_add(&N.bal[et], fo - fn);
+        ch = true;
+      }
+    }
+    wappend(ch, et, N.touch, ntouch);
+    wappend(ch, eh, N.touch, ntouch);
+  }
+  suml = wsum128(suml);
+  sumu = wsum128(sumu);
+  ninf = wsum(ninf);
+  max_inf_f = wmax(max_inf_f);
+  // infinity_sentinel (flow.hpp:58-68) and the aux total (flow.hpp:196-197)
+  const i128 sent128 = suml + sumu + 1;
+  if (sent128 > static_cast<i128>(LLONG_MAX / 4)) return PB_ERR_OVERFLOW;
+  N.S = static_cast<long long>(sent128);
+  const i128 aux = sumu + static_cast<i128>(ninf) * N.S + suml;
+  if (aux + 1 > static_cast<i128>(LLONG_MAX / 2)) return PB_ERR_OVERFLOW;
+  __syncwarp();
+  if (max_inf_f > N.S) {
+    // a carried flow exceeds the shrunken sentinel: clamp infinite edges
+    const int nedges = n + I.ne;
+    for (int base = 0; base < nedges; base += 32) {
+      const int k = base + ln;
+      bool ch = false;
+      int a = 0, b = 0;
+      if (k < nedges && W.ecrit[k]) {
+        const bool inf = k >= n || W.cap[k].y < 0;
+        const int2 ps = I.epos[k];
+        const long long f = -N.resid[ps.x] - 1;
+        if (inf && f > N.S) {
+          const long long lo = k < n ? W.cap[k].x : 0;
+          N.resid[ps.x] = -(N.S + 1);
+          N.resid[ps.y] = N.S - lo;
+          if (k < n) {
+            a = 2 * k;
+            b = 2 * k + 1;
+          } else {
+            const int2 uv = I.dep_nd[k - n];
+            a = ec_tail_of(n, uv.x);
+            b = ec_head_of(n, uv.y);
+          }
+          red_add(&N.bal[b], N.S - f);
+          red_add(&N.bal[a], f - N.S);
+          ch = true;
+        }
+      }
+      wappend(ch, a, N.touch, ntouch);
+      wappend(ch, b, N.touch, ntouch);
+    }
+  }
+  __syncwarp();
+  C.add(kPrCap, now() - t0);
+  return PB_OK;
 }
 
 __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& pool, Counters& C) {
   const int ln = lane_id();
   const int n = I.n;
-  N.V = 2 * n + 2;
+  N.V = I.V;
   N.src = 2 * n;
   N.snk = 2 * n + 1;
-  N.ret = n + I.ne;
-  N.E = n + I.ne + 1;
+  N.ret_pt = I.ret_pt;
+  N.ret_ph = I.ret_ph;
+  N.nbitw = (I.V + 31) >> 5;
   N.inc_off = I.inc_off;
-  N.inc = I.inc;
-  N.tail = I.ec_tail;
-  N.head = I.ec_head;
-  reset_net(N);
+  N.ient = I.ient;
+  N.S = 0;
+  N.R = 0;
+  for (int p = ln; p < 2 * I.E; p += 32) N.resid[p] = 0;
+  for (int v = ln; v < I.V; v += 32) N.bal[v] = 0;
+  for (int e = ln; e < I.E; e += 32) W.ecrit[e] = 0;
 
   int bad = 0;
   long long spe = 0, spt = 0, sre = 0, srt = 0;
+  // all-max durations (emulator.hpp:140-149) first, for T_min
+  for (int i = ln; i < n; i += 32) W.durr[i] = I.pt_time[I.cls_pt_off[I.comp_class[i]]];
+  __syncwarp();
+  long long t_min, unused;
+  sweep(I, W.durr, W.durr, W.fin, W.tl, false, t_min, unused, C);
   for (int i = ln; i < n; i += 32) {
     const int c = I.comp_class[i];
     long long t;
@@ -501,15 +711,14 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       t = I.start_planned_t[i];
     else
       t = I.cls_const[c] ? I.pt_time[I.cls_pt_off[c]] : I.cls_tmax[c];
-    W.planned[i] = t;
+    W.durp[i] = t;
     const int ch = discretize_choice(I, c, t);
     W.choice[i] = static_cast<uint8_t>(ch);
-    W.rdur[i] = I.pt_time[I.cls_pt_off[c] + ch];
-    W.pdur[i] = I.pt_time[I.cls_pt_off[c]];  // all-max durations (emulator.hpp:140-149)
+    W.durr[i] = I.pt_time[I.cls_pt_off[c] + ch];
     spe += table_energy(I, c, t, &bad);
     spt += t;
     sre += I.pt_energy[I.cls_pt_off[c] + ch];
-    srt += W.rdur[i];
+    srt += W.durr[i];
   }
   __syncwarp();
   spe = wsum(spe);
@@ -518,10 +727,8 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   srt = wsum(srt);
 
   const long long t_walk0 = now();
-  int detail = 0;
-  const long long t_min = forward_pass(I, W.pdur, W.estart, C);
-  long long t_cur = forward_pass(I, W.planned, W.estart, C);
-  long long t_real = forward_pass(I, W.rdur, W.rstart, C);
+  long long t_cur, t_real;
+  sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_cur, t_real, C);
   const long long t_star = t_cur;
   if (ln == 0) write_point(I, 0, t_cur, t_real, spe, spt, sre, srt, 0, 0, 0, 0, 0);
   int steps = 0;
@@ -549,151 +756,53 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       status = kStatusLogFull;
       break;
     }
-    // ---- K2 backward pass (latest) on the current planned durations
-    backward_pass(I, W.planned, W.lend, t_cur, C);
-    // ---- K3 critical mask + capacities; carried flow clamped into the new bounds
-    const long long tcap = now();
-    C.add(kPrSteps, 1);
-    i128 suml = 0, sumu = 0;
-    long long ninf = 0, max_inf_f = 0;
+    // ---- K3 critical network + capacities, carried flow clamped into the new bounds
     int ntouch = 0;
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + ln;
-      bool ch = false;
-      if (i < n) {
-        const int c = I.comp_class[i];
-        const long long t = W.planned[i];
-        const bool crit = W.estart[i] + t == W.lend[i];
-        long long l = 0, u = 0;
-        uint8_t inf = 1;
-        if (crit && !I.cls_const[c]) {
-          const long long tmin = I.cls_tmin[c], tmax = I.cls_tmax[c];
-          const bool can_speed = t - step >= tmin;
-          const bool can_slow = t + step <= tmax;
-          const double et = (can_speed || can_slow) ? table_at(I, c, t, &bad) : 0.0;
-          if (can_slow) {
-            const long long r = llround(et - table_at(I, c, t + step, &bad));
-            l = r > 0 ? r : 0;
-          }
-          if (can_speed) {
-            const long long r = llround(table_at(I, c, t - step, &bad) - et);
-            u = r > l ? r : l;
-            inf = 0;
-          }
-        }
-        const long long fo = N.f[i];
-        long long fn = 0;
-        if (crit) {
-          fn = fo < l ? l : fo;
-          if (!inf && fn > u) fn = u;
-          suml += l;
-          if (!inf)
-            sumu += u;
-          else {
-            ++ninf;
-            max_inf_f = fn > max_inf_f ? fn : max_inf_f;
-          }
-        }
-        N.lo[i] = l;
-        N.up[i] = u;
-        N.inf[i] = inf;
-        N.crit[i] = crit;
-        if (fn != fo) {
-          N.f[i] = fn;
-          flow_change(N, i, fn - fo);
-          ch = true;
-        }
-      }
-      wappend(ch, 2 * i, N.touch, ntouch);
-      wappend(ch, 2 * i + 1, N.touch, ntouch);
-    }
-    for (int base = 0; base < I.ne; base += 32) {
-      const int j = base + ln;
-      bool ch = false;
-      const int k = n + j;
-      if (j < I.ne) {
-        const int u = I.dep_tail[j], v = I.dep_head[j];
-        long long te, he;
-        bool tc, hc;
-        if (u == n) {
-          te = 0;
-          tc = true;  // latest[source] == 0 whenever a critical head exists
-        } else {
-          te = W.estart[u] + W.planned[u];
-          tc = te == W.lend[u];
-        }
-        if (v == n + 1) {
-          he = t_cur;
-          hc = true;
-        } else {
-          he = W.estart[v];
-          hc = W.estart[v] + W.planned[v] == W.lend[v];
-        }
-        const bool crit = tc && hc && te == he;
-        N.crit[k] = crit;
-        N.lo[k] = 0;
-        N.inf[k] = 1;
-        const long long fo = N.f[k];
-        if (crit) {
-          ++ninf;
-          max_inf_f = fo > max_inf_f ? fo : max_inf_f;
-        } else if (fo != 0) {
-          N.f[k] = 0;
-          flow_change(N, k, -fo);
-          ch = true;
-        }
-      }
-      wappend(ch, ch ? N.tail[k] : 0, N.touch, ntouch);
-      wappend(ch, ch ? N.head[k] : 0, N.touch, ntouch);
-    }
-    suml = wsum128(suml);
-    sumu = wsum128(sumu);
-    ninf = wsum(ninf);
-    max_inf_f = wmax(max_inf_f);
-    // infinity_sentinel (flow.hpp:58-68) and the aux total (flow.hpp:196-197)
-    const i128 sent128 = suml + sumu + 1;
-    if (sent128 > static_cast<i128>(LLONG_MAX / 4)) {
-      status = PB_ERR_OVERFLOW;
+    const int cs = build_caps(I, N, W, step, t_cur, ntouch, &bad, C);
+    if (cs != PB_OK) {
+      status = cs;
       break;
     }
-    N.sentinel = static_cast<long long>(sent128);
-    const i128 aux = sumu + static_cast<i128>(ninf) * N.sentinel + suml;
-    if (aux + 1 > static_cast<i128>(LLONG_MAX / 2)) {
-      status = PB_ERR_OVERFLOW;
-      break;
-    }
-    __syncwarp();
-    if (max_inf_f > N.sentinel) clamp_infinite(N, nedges, ntouch);
-    C.add(kPrCap, now() - tcap);
     // ---- K4 warm-started max flow with lower bounds
     if (!repair(N, ntouch, C)) {
       stop = PB_STOP_INFEASIBLE;
       break;
     }
     maximize(N, C);
-    if (N.f[N.ret] >= N.sentinel) {
+    if (N.R >= N.S) {
       stop = PB_STOP_INFINITE_CUT;
       break;
     }
     // ---- K5 minimal min cut = the last BFS's visited set
     const long long tupd = now();
-    const int side_stamp = N.stamp;
     long long cost = 0;
     int nd = 0;
     for (int base = 0; base < nedges; base += 32) {
       const int k = base + ln;
       int rec = 0;
-      if (k < nedges && N.crit[k]) {
-        const bool a = N.vis[N.tail[k]] == side_stamp, b = N.vis[N.head[k]] == side_stamp;
-        if (a && !b) {
-          cost += N.inf[k] ? N.sentinel : N.up[k];
-          if (k < n) rec = k + 1;
-        } else if (!a && b) {
-          cost -= N.lo[k];
+      if (k < nedges && W.ecrit[k]) {
+        int a, b;
+        if (k < n) {
+          a = 2 * k;
+          b = 2 * k + 1;
+        } else {
+          const int2 uv = I.dep_nd[k - n];
+          a = ec_tail_of(n, uv.x);
+          b = ec_head_of(n, uv.y);
+        }
+        const bool sa = bit_of(N, a), sb = bit_of(N, b);
+        if (sa && !sb) {
           if (k < n) {
-            const int c = I.comp_class[k];
-            if (!I.cls_const[c] && W.planned[k] + step <= I.cls_tmax[c]) rec = -(k + 1);
+            const long long u = W.cap[k].y;
+            cost += u < 0 ? N.S : u;
+            rec = k + 1;
+          } else {
+            cost += N.S;
           }
+        } else if (!sa && sb && k < n) {
+          cost -= W.cap[k].x;
+          const int c = I.comp_class[k];
+          if (!I.cls_const[c] && W.durp[k] + step <= I.cls_tmax[c]) rec = -(k + 1);
         }
       }
       wappend(rec != 0, rec, W.delta, nd);
@@ -708,21 +817,23 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       status = kStatusLogFull;
       break;
     }
-    // order: sped ascending, then slowed ascending (frontier.hpp:111-125)
+    // order: sped ascending, then slowed ascending, by caller id (frontier.hpp:111-125)
     int ns_loc = 0;
     long long dpe = 0, dpt = 0, dre = 0, drt = 0;
     for (int q = ln; q < nd; q += 32) {
       const int x = W.delta[q];
-      const long long kx = x > 0 ? x : (1ll << 40) - x;
+      const int i = (x > 0 ? x : -x) - 1;
+      const int oi = I.orig[i];
+      const long long kx = x > 0 ? oi : (1ll << 40) + oi;
       int rank = 0;
       for (int r = 0; r < nd; ++r) {
         const int y = W.delta[r];
-        const long long ky = y > 0 ? y : (1ll << 40) - y;
+        const int oj = I.orig[(y > 0 ? y : -y) - 1];
+        const long long ky = y > 0 ? oj : (1ll << 40) + oj;
         rank += ky < kx;
       }
-      const int i = (x > 0 ? x : -x) - 1;
       const int c = I.comp_class[i];
-      const long long told = W.planned[i];
+      const long long told = W.durp[i];
       const long long tnew = x > 0 ? told - step : told + step;
       const long long eold = table_energy(I, c, told, &bad);
       const long long enew = table_energy(I, c, tnew, &bad);
@@ -734,7 +845,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       dre += I.pt_energy[p0 + chnew] - I.pt_energy[p0 + chold];
       drt += I.pt_time[p0 + chnew] - I.pt_time[p0 + chold];
       ns_loc += x > 0;
-      pool.ids[at + rank] = x;
+      pool.ids[at + rank] = x > 0 ? oi + 1 : -(oi + 1);
       pool.choice[at + rank] = static_cast<uint8_t>(chnew);
     }
     __syncwarp();
@@ -742,11 +853,11 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       const int x = W.delta[q];
       const int i = (x > 0 ? x : -x) - 1;
       const int c = I.comp_class[i];
-      const long long tnew = x > 0 ? W.planned[i] - step : W.planned[i] + step;
-      W.planned[i] = tnew;
+      const long long tnew = x > 0 ? W.durp[i] - step : W.durp[i] + step;
+      W.durp[i] = tnew;
       const int ch = discretize_choice(I, c, tnew);
       W.choice[i] = static_cast<uint8_t>(ch);
-      W.rdur[i] = I.pt_time[I.cls_pt_off[c] + ch];
+      W.durr[i] = I.pt_time[I.cls_pt_off[c] + ch];
     }
     __syncwarp();
     const int ns = static_cast<int>(wsum(ns_loc));
@@ -755,8 +866,10 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     dre = wsum(dre);
     drt = wsum(drt);
     C.add(kPrUpdate, now() - tupd);
-    // refresh_totals (frontier.hpp:64-67): new planned makespan
-    const long long t_new = forward_pass(I, W.planned, W.estart, C);
+    // refresh_totals (frontier.hpp:64-67) + discretize (frontier.hpp:157):
+    // planned and realized makespans and the next step's tails, one sweep
+    long long t_new;
+    sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_new, t_real, C);
     if (I.mode == kModeDiscover && t_new >= t_cur) {
       stop = PB_STOP_NO_PROGRESS;
       break;
@@ -766,8 +879,6 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     spt += dpt;
     sre += dre;
     srt += drt;
-    // discretize (frontier.hpp:157): realized makespan
-    t_real = forward_pass(I, W.rdur, W.rstart, C);
     ++steps;
     if (ln == 0)
       write_point(I, steps, t_cur, t_real, spe, spt, sre, srt, cost, step, static_cast<int>(at), ns, nd - ns);
@@ -785,7 +896,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     s.status = status;
     s.n_ids = static_cast<int32_t>(n_ids);
     s.n_extrapolated = static_cast<int32_t>(n_extrap);
-    s.pad = detail;
+    s.pad = 0;
     *I.summary = s;
   }
   __syncwarp();
@@ -796,29 +907,27 @@ struct WsPtrs {
   Walk W;
 };
 
-__device__ WsPtrs bind_ws(char* base, const WsLayout& L) {
+__device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   WsPtrs p;
-  p.N.lo = reinterpret_cast<int64_t*>(base + L.off_lo);
-  p.N.up = reinterpret_cast<int64_t*>(base + L.off_up);
-  p.N.f = reinterpret_cast<int64_t*>(base + L.off_f);
-  p.N.inf = reinterpret_cast<uint8_t*>(base + L.off_inf);
-  p.N.crit = reinterpret_cast<uint8_t*>(base + L.off_crit);
-  p.N.bal = reinterpret_cast<int64_t*>(base + L.off_bal);
-  p.N.vis = reinterpret_cast<int32_t*>(base + L.off_vis);
-  p.N.par = reinterpret_cast<int32_t*>(base + L.off_par);
-  p.N.mk = reinterpret_cast<int32_t*>(base + L.off_mk);
-  p.N.f0 = reinterpret_cast<int32_t*>(base + L.off_f0);
-  p.N.f1 = reinterpret_cast<int32_t*>(base + L.off_f1);
+  p.N.resid = reinterpret_cast<long long*>(base + L.off_resid);
+  p.N.bal = reinterpret_cast<long long*>(base + L.off_bal);
+  p.N.lg = reinterpret_cast<int2*>(base + L.off_log);
+  p.N.fglob = reinterpret_cast<int4*>(base + L.off_front);
+  p.N.fstride = static_cast<int>(L.max_v);
+  p.N.path = reinterpret_cast<int32_t*>(base + L.off_path);
   p.N.touch = reinterpret_cast<int32_t*>(base + L.off_touch);
   p.N.exl = reinterpret_cast<int32_t*>(base + L.off_exl);
-  p.W.planned = reinterpret_cast<int64_t*>(base + L.off_planned);
-  p.W.estart = reinterpret_cast<int64_t*>(base + L.off_estart);
-  p.W.lend = reinterpret_cast<int64_t*>(base + L.off_lend);
-  p.W.rstart = reinterpret_cast<int64_t*>(base + L.off_rstart);
-  p.W.rdur = reinterpret_cast<int64_t*>(base + L.off_rdur);
-  p.W.pdur = reinterpret_cast<int64_t*>(base + L.off_pdur);
+  p.W.durp = reinterpret_cast<long long*>(base + L.off_durp);
+  p.W.durr = reinterpret_cast<long long*>(base + L.off_durr);
+  p.W.fin = reinterpret_cast<longlong2*>(base + L.off_fin);
+  p.W.tl = reinterpret_cast<longlong2*>(base + L.off_hl);
+  p.W.cap = reinterpret_cast<longlong2*>(base + L.off_cap);
+  p.W.ecrit = reinterpret_cast<uint8_t*>(base + L.off_ecrit);
   p.W.choice = reinterpret_cast<uint8_t*>(base + L.off_choice);
   p.W.delta = reinterpret_cast<int32_t*>(base + L.off_delta);
+  // shared memory: frontier (16 B aligned) then bitset
+  p.N.fs = reinterpret_cast<int4*>(smem);
+  p.N.bits = reinterpret_cast<uint32_t*>(smem + 16 * 2 * kFrontCap);
   return p;
 }
 
@@ -836,8 +945,19 @@ __device__ void flush_counters(const Counters& C, RunCounters* out) {
   }
 }
 
-__device__ __forceinline__ int warp_slot() {
-  return blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+__device__ __forceinline__ int warp_in_block() { return threadIdx.x >> 5; }
+__device__ __forceinline__ int warp_slot() { return blockIdx.x * kWarpsPerBlock + warp_in_block(); }
+
+// Per-warp shared memory: [profile 16 x u64][frontier + bitset].
+extern __shared__ __align__(16) char g_smem[];
+
+__device__ __forceinline__ char* my_smem(const WsLayout& L, unsigned long long** prof) {
+  const int per = 128 + L.smem_bytes;
+  char* base = g_smem + warp_in_block() * per;
+  *prof = reinterpret_cast<unsigned long long*>(base);
+  if (lane_id() < kPrSlots) (*prof)[lane_id()] = 0;
+  __syncwarp();
+  return base + 128;
 }
 
 __global__ void __launch_bounds__(kBlock) walk_kernel(const DevInst* insts, int n_inst,
@@ -846,8 +966,9 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const DevInst* insts, int 
                                                       RunCounters* ctr, DeltaPool pool) {
   const int slot = warp_slot();
   if (slot >= slots) return;
-  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(slot) * L.stride, L);
   Counters C;
+  char* sm = my_smem(L, &C.prof);
+  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(slot) * L.stride, L, sm);
   for (;;) {
     int k = 0;
     if (lane_id() == 0) k = atomicAdd(counter, 1);
@@ -866,58 +987,63 @@ __global__ void __launch_bounds__(kBlock) flow_kernel(const DevFlowJob* jobs, in
                                                       char* ws_base, WsLayout L, int slots) {
   const int slot = warp_slot();
   if (slot >= slots) return;
-  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(slot) * L.stride, L);
-  Net& N = P.N;
   Counters C;
+  char* sm = my_smem(L, &C.prof);
+  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(slot) * L.stride, L, sm);
+  Net& N = P.N;
   const int ln = lane_id();
   for (int g = slot; g < count; g += slots) {
     const DevFlowJob& J = jobs[g];
     N.V = J.nodes;
     N.src = J.source;
     N.snk = J.sink;
-    N.ret = J.m;
-    N.E = J.m + 1;
+    N.ret_pt = J.ret_pt;
+    N.ret_ph = J.ret_ph;
+    N.nbitw = (J.nodes + 31) >> 5;
     N.inc_off = J.inc_off;
-    N.inc = J.inc;
-    N.tail = J.tail;
-    N.head = J.head;
-    reset_net(N);
+    N.ient = J.ient;
+    N.R = 0;
+    for (int p = ln; p < 2 * (J.m + 1); p += 32) N.resid[p] = 0;
+    for (int v = ln; v < J.nodes; v += 32) N.bal[v] = 0;
+    __syncwarp();
     i128 suml = 0, sumu = 0;
     long long ninf = 0;
     int ntouch = 0;
     for (int base = 0; base < J.m; base += 32) {
       const int e = base + ln;
       bool ch = false;
+      int a = 0, b = 0;
       if (e < J.m) {
-        N.lo[e] = J.lower[e];
-        N.up[e] = J.upper[e];
-        N.inf[e] = J.inf[e];
-        N.crit[e] = 1;
-        suml += J.lower[e];
+        const long long l = J.lower[e];
+        const int2 ps = J.epos[e];
+        N.resid[ps.x] = J.inf[e] ? -(l + 1) : J.upper[e] - l;
+        N.resid[ps.y] = 0;
+        suml += l;
         if (!J.inf[e])
           sumu += J.upper[e];
         else
           ++ninf;
-        if (J.lower[e] > 0) {
-          N.f[e] = J.lower[e];
-          flow_change(N, e, J.lower[e]);
+        if (l > 0) {
+          a = J.tail[e];
+          b = J.head[e];
+          red_add(&N.bal[b], l);
+          red_add(&N.bal[a], -l);
           ch = true;
         }
       }
-      wappend(ch, ch ? J.tail[e] : 0, N.touch, ntouch);
-      wappend(ch, ch ? J.head[e] : 0, N.touch, ntouch);
+      wappend(ch, a, N.touch, ntouch);
+      wappend(ch, b, N.touch, ntouch);
     }
     suml = wsum128(suml);
     sumu = wsum128(sumu);
     ninf = wsum(ninf);
     const i128 sent128 = suml + sumu + 1;
     int status = PB_OK;
-    i128 aux = 0;
     if (sent128 > static_cast<i128>(LLONG_MAX / 4)) {
       status = PB_ERR_OVERFLOW;
     } else {
-      N.sentinel = static_cast<long long>(sent128);
-      aux = sumu + static_cast<i128>(ninf) * N.sentinel + suml;
+      N.S = static_cast<long long>(sent128);
+      const i128 aux = sumu + static_cast<i128>(ninf) * N.S + suml;
       if (aux + 1 > static_cast<i128>(LLONG_MAX / 2)) status = PB_ERR_OVERFLOW;
     }
     __syncwarp();
@@ -933,19 +1059,18 @@ __global__ void __launch_bounds__(kBlock) flow_kernel(const DevFlowJob* jobs, in
       if (ln == 0) {
         J.status[g] = PB_OK;
         J.feasible[g] = 0;
-        J.sentinel[g] = N.sentinel;
+        J.sentinel[g] = N.S;
       }
       __syncwarp();
       continue;
     }
     maximize(N, C);
-    const int side_stamp = N.stamp;
     long long cost = 0;
     for (int e = ln; e < J.m; e += 32) {
-      const bool a = N.vis[N.tail[e]] == side_stamp, b = N.vis[N.head[e]] == side_stamp;
+      const bool a = bit_of(N, J.tail[e]), b = bit_of(N, J.head[e]);
       int8_t dir = 0;
       if (a && !b) {
-        cost += J.inf[e] ? N.sentinel : J.upper[e];
+        cost += J.inf[e] ? N.S : J.upper[e];
         dir = 1;
       } else if (!a && b) {
         cost -= J.lower[e];
@@ -953,13 +1078,13 @@ __global__ void __launch_bounds__(kBlock) flow_kernel(const DevFlowJob* jobs, in
       }
       J.cut_dir[e] = dir;
     }
-    for (int v = ln; v < N.V; v += 32) J.side[v] = N.vis[v] == side_stamp ? 1 : 0;
+    for (int v = ln; v < N.V; v += 32) J.side[v] = bit_of(N, v) ? 1 : 0;
     cost = wsum(cost);
     if (ln == 0) {
-      J.status[g] = N.vis[N.snk] == side_stamp ? PB_ERR_LOGIC : PB_OK;
+      J.status[g] = bit_of(N, N.snk) ? PB_ERR_LOGIC : PB_OK;
       J.feasible[g] = 1;
-      J.value[g] = N.f[N.ret];
-      J.sentinel[g] = N.sentinel;
+      J.value[g] = N.R;
+      J.sentinel[g] = N.S;
       J.cost[g] = cost;
     }
     __syncwarp();
@@ -968,35 +1093,45 @@ __global__ void __launch_bounds__(kBlock) flow_kernel(const DevFlowJob* jobs, in
 
 // ------------------------------------------------------------ slack jobs
 
+// annotate_slack (dag.hpp:233-286) through the fused sweep; outputs in the
+// caller's ids.
 __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, const SlackOut* outs,
                                                        int64_t* makespan, int count, char* ws_base,
                                                        WsLayout L, int slots) {
   const int slot = warp_slot();
   if (slot >= slots) return;
-  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(slot) * L.stride, L);
   Counters C;
+  char* sm = my_smem(L, &C.prof);
+  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(slot) * L.stride, L, sm);
+  Walk& W = P.W;
   const int ln = lane_id();
   for (int g = slot; g < count; g += slots) {
     const DevInst& I = insts[g];
     const SlackOut& O = outs[g];
     const int n = I.n;
-    const long long ms = forward_pass(I, O.dur, P.W.estart, C);
-    backward_pass(I, O.dur, P.W.lend, ms, C);
-    // latest of the source node: min over source out-edges of latest[2v]
+    for (int i = ln; i < n; i += 32) W.durp[i] = O.dur[I.orig[i]];
+    __syncwarp();
+    long long ms, unused;
+    sweep(I, W.durp, W.durp, W.fin, W.tl, true, ms, unused, C);
+    __syncwarp();
+    // latest of the source node: min over its successors' latest start
     long long ls = ms;
-    for (int j = ln; j < I.ne; j += 32)
-      if (I.dep_tail[j] == n && I.dep_head[j] < n) {
-        const int v = I.dep_head[j];
-        const long long c = P.W.lend[v] - O.dur[v];
+    for (int j = ln; j < I.ne; j += 32) {
+      const int2 uv = I.dep_nd[j];
+      if (uv.x == n && uv.y < n) {
+        const long long c = ms - W.tl[uv.y].x;
         if (c < ls) ls = c;
       }
+    }
     ls = wmin(ls);
     for (int i = ln; i < n; i += 32) {
-      O.earliest[2 * i] = P.W.estart[i];
-      O.earliest[2 * i + 1] = P.W.estart[i] + O.dur[i];
-      O.latest[2 * i + 1] = P.W.lend[i];
-      O.latest[2 * i] = P.W.lend[i] - O.dur[i];
-      O.critical[i] = P.W.estart[i] + O.dur[i] == P.W.lend[i];
+      const int o = I.orig[i];
+      const long long d = W.durp[i], f = W.fin[i].x, h = W.tl[i].x;
+      O.earliest[2 * o] = f - d;
+      O.earliest[2 * o + 1] = f;
+      O.latest[2 * o + 1] = ms - (h - d);
+      O.latest[2 * o] = ms - h;
+      O.critical[o] = f + h - d == ms;
     }
     if (ln == 0) {
       O.earliest[2 * n] = 0;
@@ -1006,21 +1141,21 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
       makespan[g] = ms;
     }
     for (int j = ln; j < I.ne; j += 32) {
-      const int u = I.dep_tail[j], v = I.dep_head[j];
+      const int2 uv = I.dep_nd[j];
       long long te, tl, he, hl;
-      if (u == n) {
+      if (uv.x == n) {
         te = 0;
         tl = ls;
       } else {
-        te = P.W.estart[u] + O.dur[u];
-        tl = P.W.lend[u];
+        te = W.fin[uv.x].x;
+        tl = ms - (W.tl[uv.x].x - W.durp[uv.x]);
       }
-      if (v == n + 1) {
+      if (uv.y == n + 1) {
         he = ms;
         hl = ms;
       } else {
-        he = P.W.estart[v];
-        hl = P.W.lend[v] - O.dur[v];
+        he = W.fin[uv.y].x - W.durp[uv.y];
+        hl = ms - W.tl[uv.y].x;
       }
       O.critical[n + j] = te == tl && he == hl && te == he;
     }
@@ -1029,33 +1164,47 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
 }
 
 int blocks_for(int slots) { return (slots + kWarpsPerBlock - 1) / kWarpsPerBlock; }
+size_t block_smem(const WsLayout& L) { return static_cast<size_t>(kWarpsPerBlock) * (128 + L.smem_bytes); }
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
 
 }  // namespace
 
-int walk_slots_per_sm() {
+int walk_slots_per_sm(const WsLayout& ws) {
+  const size_t sm = block_smem(ws);
+  set_smem(walk_kernel, sm);
   int blocks = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, walk_kernel, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, walk_kernel, kBlock, sm);
   return blocks * kWarpsPerBlock;
 }
 
 int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
                  char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
                  DeltaPool pool, void* stream) {
-  walk_kernel<<<blocks_for(slots), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+  const size_t sm = block_smem(ws);
+  set_smem(walk_kernel, sm);
+  walk_kernel<<<blocks_for(slots), kBlock, sm, static_cast<cudaStream_t>(stream)>>>(
       d_insts, n_inst, d_order, d_counter, d_ws, ws, slots, d_counters, pool);
   return static_cast<int>(cudaGetLastError());
 }
 
 int launch_flow_jobs(const DevFlowJob* d_jobs, int32_t count, char* d_ws, const WsLayout& ws,
                      int32_t slots, void* stream) {
-  flow_kernel<<<blocks_for(slots), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(d_jobs, count, d_ws,
-                                                                                   ws, slots);
+  const size_t sm = block_smem(ws);
+  set_smem(flow_kernel, sm);
+  flow_kernel<<<blocks_for(slots), kBlock, sm, static_cast<cudaStream_t>(stream)>>>(d_jobs, count, d_ws,
+                                                                                    ws, slots);
   return static_cast<int>(cudaGetLastError());
 }
 
 int launch_slack_jobs(const DevInst* d_insts, const SlackOut* d_outs, int64_t* d_makespan,
                       int32_t count, char* d_ws, const WsLayout& ws, int32_t slots, void* stream) {
-  slack_kernel<<<blocks_for(slots), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+  const size_t sm = block_smem(ws);
+  set_smem(slack_kernel, sm);
+  slack_kernel<<<blocks_for(slots), kBlock, sm, static_cast<cudaStream_t>(stream)>>>(
       d_insts, d_outs, d_makespan, count, d_ws, ws, slots);
   return static_cast<int>(cudaGetLastError());
 }
