@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libperseus_b200.so")
+# PB_LIB_VARIANT selects an experimental build (_lib/libperseus_b200<variant>.so) for A/B timing.
+LIB_PATH = os.path.join(_HERE, "_lib", f"libperseus_b200{os.environ.get('PB_LIB_VARIANT', '')}.so")
 
 PB_OK = 0
 PB_ERR_INVALID_ARGUMENT = 1

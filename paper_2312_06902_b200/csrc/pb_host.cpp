@@ -365,7 +365,7 @@ struct Packed {
 enum OffIdx {
   O_ORIG, O_CLASS, O_CFLAG, O_LVLOFF, O_FROW, O_BROW, O_PINOFF, O_PIN, O_POUTOFF, O_POUT, O_DEPND,
   O_INCOFF, O_IENT, O_EPOS, O_CCONST, O_CTMIN, O_CTMAX, O_CTAB, O_CPOFF, O_PTIME, O_PENERGY,
-  O_START, O_CURVE, O_POINTS, O_SUMMARY, O_COUNT
+  O_START, O_CURVE, O_CREC, O_POINTS, O_SUMMARY, O_COUNT
 };
 
 void put_static(Blob& blob, const HostInst& h, std::array<size_t, 32>& o) {
@@ -453,6 +453,16 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
     o[O_PENERGY] = P.stat.put(h.pt_energy);
     o[O_START] = h.istart.empty() ? SIZE_MAX : P.stat.put(h.istart);
     o[O_CURVE] = P.stat.put(h.cls_curve);
+    {
+      std::vector<pb::CompRec> rec(h.n);
+      for (int32_t i = 0; i < h.n; ++i) {
+        const int32_t c = h.icls[i];
+        const bool cst = h.cls_const[c] != 0;
+        rec[i] = pb::CompRec{cst ? 0 : h.cls_trange[2 * c], cst ? 0 : h.cls_trange[2 * c + 1],
+                             cst ? -1 : b->cls_tab[k][c], h.net.epos[i].x, h.net.epos[i].y};
+      }
+      o[O_CREC] = P.stat.put(rec);
+    }
     const int64_t est = static_cast<int64_t>(static_cast<double>(h.est_steps) * cap_scale);
     cap_points[k] = static_cast<int32_t>(std::min<int64_t>(est + 8, INT32_MAX / 2));
     pool += est * 12 + 2 * int64_t{h.n} + 64;
@@ -527,6 +537,7 @@ void bind_device(Packed& P, char* d_static, char* d_out, size_t tables_off) {
     d.tables = dptr<double>(d_static, tables_off);
     d.start_planned_t = dptr<int64_t>(d_static, o[O_START]);
     d.cls_curve = dptr<double>(d_static, o[O_CURVE]);
+    d.crec = dptr<pb::CompRec>(d_static, o[O_CREC]);
     d.points = dptr<pb_point>(d_out, o[O_POINTS]);
     d.summary = dptr<pb_frontier_summary>(d_out, o[O_SUMMARY]);
   }

@@ -33,6 +33,14 @@ struct IEnt {
   int32_t other_end;
 };
 
+// Per-computation static record for the capacity build (32 B): the class's
+// curve interval, its table offset (tab < 0: constant class) and the
+// computation edge's two incidence positions.
+struct CompRec {
+  int64_t tmin, tmax, tab;
+  int32_t pt, ph;
+};
+
 // Host mirrors of the int2 / int4 layouts (no CUDA headers needed).
 struct int2h {
   int32_t x, y;
@@ -82,6 +90,7 @@ struct DevInst {
   const int32_t* inc_off;     // [V + 1]
   const IEnt* ient;           // [2E]
   const int2* epos;           // [E] {position at tail, position at head}
+  const CompRec* crec;        // [n]
   // cost model
   const uint8_t* cls_const;   // [classes]
   const int64_t* cls_tmin;    // [classes] curve t_min (table origin)
@@ -131,7 +140,7 @@ struct WsLayout {
   int64_t off_hl;                      // int64x2 [n] {planned duration + tail, 0}
   int64_t off_fin;                     // int64x2 [n] {finish planned, finish realized}
   int64_t off_cap;                     // int64x2 [n] {lower, upper (-1 = infinite)}
-  int64_t off_ccrit, off_choice;       // u8 [n]
+  int64_t off_ccrit, off_choice;       // u8 [n] (off_ccrit: dirty flags)
   int64_t off_touch, off_exl, off_delta, off_path;  // int32 lists
   int64_t stride;
   int32_t smem_bytes;  // dynamic shared memory per warp

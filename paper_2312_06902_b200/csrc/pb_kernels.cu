@@ -44,8 +44,13 @@ namespace {
 
 constexpr int kWarpsPerBlock = 4;
 constexpr int kBlock = 32 * kWarpsPerBlock;
+#ifndef PB_MIN_BLOCKS
+#define PB_MIN_BLOCKS 3
+#endif
+constexpr int kMinBlocks = PB_MIN_BLOCKS;  // walker blocks per SM the register budget must allow
 constexpr unsigned kFull = 0xffffffffu;
 constexpr long long kHuge = LLONG_MAX / 4;  // return-arc capacity (never binding)
+constexpr int kMaxEnds = 32;               // phase-B path ends kept per BFS
 typedef __int128 i128;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -122,8 +127,9 @@ struct Net {
   long long* bal;
   int2* lg;        // BFS log: {position used to reach the node, parent log index}
   int4* fglob;     // frontier overflow, 2 buffers of fstride entries
-  uint32_t* bits;  // smem visited bitset
-  int4* fs;        // smem frontier, 2 buffers of kFrontCap entries
+  uint32_t s_bits;  // smem (shared-window address) visited bitset
+  uint32_t s_fs;    // smem frontier, 2 buffers of kFrontCap int4 entries
+  int2* ends;       // smem: phase-B arcs into the sink {position, parent log index}
   int32_t* path;
   int32_t* touch;
   int32_t* exl;
@@ -131,141 +137,254 @@ struct Net {
   long long R;  // flow on the return arc = s->t value
 };
 
-__device__ __forceinline__ int4* fslot(const Net& N, int buf, int k) {
-  return k < kFrontCap ? &N.fs[buf * kFrontCap + k] : &N.fglob[static_cast<size_t>(buf) * N.fstride + k];
+// Explicit shared-memory accessors (the smem base travels in a struct, so
+// plain pointers would compile to generic LD/ST).
+__device__ __forceinline__ int4 lds128(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, int4 v) {
+  asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atoms_or(uint32_t a, uint32_t m) {
+  uint32_t old;
+  asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(m) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ int4 fread(const Net& N, int buf, int k) {
+  return k < kFrontCap ? lds128(N.s_fs + 16u * (buf * kFrontCap + k))
+                       : N.fglob[static_cast<size_t>(buf) * N.fstride + k];
+}
+__device__ __forceinline__ void fwrite(const Net& N, int buf, int k, int4 v) {
+  if (k < kFrontCap)
+    sts128(N.s_fs + 16u * (buf * kFrontCap + k), v);
+  else
+    N.fglob[static_cast<size_t>(buf) * N.fstride + k] = v;
 }
 
 __device__ __forceinline__ void clear_bits(Net& N) {
-  for (int w = lane_id(); w < N.nbitw; w += 32) N.bits[w] = 0;
+  for (int w = lane_id(); w < N.nbitw; w += 32) sts32(N.s_bits + 4u * w, 0u);
   __syncwarp();
 }
 // true when this call set the bit
 __device__ __forceinline__ bool test_and_set(Net& N, int u) {
   const uint32_t m = 1u << (u & 31);
-  return (atomicOr(&N.bits[u >> 5], m) & m) == 0;
+  return (atoms_or(N.s_bits + 4u * (u >> 5), m) & m) == 0;
 }
-__device__ __forceinline__ bool bit_of(const Net& N, int u) { return (N.bits[u >> 5] >> (u & 31)) & 1u; }
+__device__ __forceinline__ bool bit_of(const Net& N, int u) {
+  return (lds32(N.s_bits + 4u * (u >> 5)) >> (u & 31)) & 1u;
+}
 
 // Seeds frontier slot k (buffer 0) and log entry k with node v.
 __device__ __forceinline__ void seed(Net& N, int k, int v) {
-  *fslot(N, 0, k) = make_int4(v, N.inc_off[v], N.inc_off[v + 1], k);
+  fwrite(N, 0, k, make_int4(v, N.inc_off[v], N.inc_off[v + 1], k));
   N.lg[k] = make_int2(-1 - v, -1);
 }
 
+// One BFS discovery: ballot-compacts the lanes whose arc p (from the
+// frontier entry with log index parent) discovered node e.other.
+__device__ __forceinline__ void discover(Net& N, bool c, int p, const IEnt& e, int parent, int nlog, int nxt,
+                                         int& nc, bool phaseA, int& found, int& tgt, unsigned& upd) {
+  const unsigned m = __ballot_sync(kFull, c);
+  if (!m) return;
+  const int pos = nc + __popc(m & lanemask_lt());
+  bool hit = false;
+  if (c) {
+    const int li = nlog + pos;
+    N.lg[li] = make_int2(p, parent);
+    fwrite(N, nxt, pos, make_int4(e.other, e.other_off, e.other_end, li));
+    if (phaseA) hit = N.bal[e.other] < 0;
+    ++upd;
+  }
+  if (phaseA) {
+    const unsigned h = __ballot_sync(kFull, hit);
+    if (h && found < 0) {
+      const int hl = __ffs(h) - 1;
+      found = __shfl_sync(kFull, nlog + pos, hl);
+      tgt = __shfl_sync(kFull, e.other, hl);
+    }
+  }
+  nc += __popc(m);
+}
+
+// Phase B: the arcs of frontier buffer buf (cnt entries) that enter the sink
+// with positive residual -> N.ends (at most kMaxEnds).
+__device__ int collect_ends(Net& N, int buf, int cnt) {
+  const int ln = lane_id();
+  const long long negS = -N.S;
+  int nend = 0;
+  for (int base = 0; base < cnt; base += 32) {
+    const int slot = base + ln;
+    int4 fe = make_int4(0, 0, 0, 0);
+    if (slot < cnt) fe = fread(N, buf, slot);
+    const int rounds = wmaxi(fe.z - fe.y);
+    for (int r = 0; r < rounds; ++r) {
+      const int p = fe.y + r;
+      bool end = false;
+      if (p < fe.z && N.ient[p].other == N.snk) {
+        const long long w = N.resid[p];
+        end = w != 0 && w >= negS;
+      }
+      const unsigned m = __ballot_sync(kFull, end);
+      const int k = nend + __popc(m & lanemask_lt());
+      if (end && k < kMaxEnds) N.ends[k] = make_int2(p, fe.w);
+      nend += __popc(m);
+    }
+  }
+  __syncwarp();
+  return nend > kMaxEnds ? kMaxEnds : nend;
+}
+
 // Level-synchronous BFS over residual arcs from the nsrc seeded sources
-// (already marked).  phaseA: targets are nodes with bal < 0; phase B: the
-// sink.  Stops after the level that reaches a target and returns its log
-// index (tgt = node); -1 when none is reachable, and then the bitset marks
-// exactly the residual-reachable set.
+// (already marked).  A lane owns 2 arcs of a round and issues both
+// {ient, resid} loads before using either; the bitset test-and-set is an
+// unconditional shared atomic (mask 0 for non-arcs).  phaseA: targets are
+// nodes with bal < 0; stops after the level that reaches one and returns
+// its log index (tgt = node).  Phase B: stops after the level that marks
+// the sink (one shared load per level) and returns the number of that
+// level's arcs into the sink, recorded in N.ends (0 = sink unreachable; the
+// bitset then marks exactly the residual-reachable set).  -1: nothing found.
 __device__ int bfs(Net& N, int nsrc, bool phaseA, int& tgt, Counters& C) {
   const int ln = lane_id();
   const long long t0 = now();
-  int cnt = nsrc, cur = 0, nlog = nsrc, found = -1;
+  const long long negS = -N.S;  // raw residual r is positive iff r != 0 && r >= -S
+  int cnt = nsrc, cur = 0, nlog = nsrc, found = -1, levels = 0, prev = 0;
+  unsigned arcs = 0, upd = 0;
   tgt = -1;
-  while (cnt > 0 && found < 0) {
-    C.add(kPrBfsLevels, 1);
+  const uint32_t snk_word = N.s_bits + 4u * (N.snk >> 5), snk_mask = 1u << (N.snk & 31);
+  while (cnt > 0) {
+    ++levels;
     const int lg2 = cnt >= 16 ? 0 : cnt >= 8 ? 1 : cnt >= 4 ? 2 : 3;  // lanes per frontier node
     const int g = 1 << lg2;
     const int sub = ln & (g - 1);
+    const int nxt = cur ^ 1;
     int nc = 0;
     for (int base = 0; base < cnt; base += 32 >> lg2) {
       const int slot = base + (ln >> lg2);
-      const bool valid = slot < cnt;
       int4 fe = make_int4(0, 0, 0, 0);
-      if (valid) fe = *fslot(N, cur, slot);
+      if (slot < cnt) fe = fread(N, cur, slot);
       const int deg = fe.z - fe.y;
       const int myr = deg > sub ? (deg - sub + g - 1) >> lg2 : 0;
       const int rounds = wmaxi(myr);
-      C.arc_scans += myr;
-      for (int r = 0; r < rounds; ++r) {
-        const int p = fe.y + sub + (r << lg2);
-        bool cand = false;
-        IEnt e{0, 0, 0, 0};
+      arcs += myr;
+      for (int r = 0; r < rounds; r += 2) {
+        const int p0 = fe.y + sub + (r << lg2), p1 = p0 + g;
+        IEnt e0{0, 0, 0, 0}, e1{0, 0, 0, 0};
+        long long w0 = 0, w1 = 0;
         if (r < myr) {
-          e = N.ient[p];
-          const long long raw = N.resid[p];
-          if (eff_res(raw, N.S) > 0) cand = test_and_set(N, e.other);
+          e0 = N.ient[p0];
+          w0 = N.resid[p0];
         }
-        const unsigned m = __ballot_sync(kFull, cand);
-        if (m) {
-          const int pos = nc + __popc(m & lanemask_lt());
-          bool hit = false;
-          if (cand) {
-            const int li = nlog + pos;
-            N.lg[li] = make_int2(p, fe.w);
-            *fslot(N, cur ^ 1, pos) = make_int4(e.other, e.other_off, e.other_end, li);
-            hit = phaseA ? N.bal[e.other] < 0 : e.other == N.snk;
-            ++C.node_updates;
-          }
-          const unsigned h = __ballot_sync(kFull, hit);
-          if (h && found < 0) {
-            const int hl = __ffs(h) - 1;
-            found = __shfl_sync(kFull, nlog + pos, hl);
-            tgt = __shfl_sync(kFull, e.other, hl);
-          }
-          nc += __popc(m);
+        if (r + 1 < myr) {
+          e1 = N.ient[p1];
+          w1 = N.resid[p1];
         }
+        const bool ok0 = w0 != 0 && w0 >= negS, ok1 = w1 != 0 && w1 >= negS;
+        const uint32_t m0 = ok0 ? 1u << (e0.other & 31) : 0u;
+        const uint32_t o0 = atoms_or(N.s_bits + 4u * (e0.other >> 5), m0);
+        const uint32_t m1 = ok1 ? 1u << (e1.other & 31) : 0u;
+        const uint32_t o1 = atoms_or(N.s_bits + 4u * (e1.other >> 5), m1);
+        discover(N, ok0 && !(o0 & m0), p0, e0, fe.w, nlog, nxt, nc, phaseA, found, tgt, upd);
+        if (r + 1 < rounds) discover(N, ok1 && !(o1 & m1), p1, e1, fe.w, nlog, nxt, nc, phaseA, found, tgt, upd);
       }
     }
     __syncwarp();
     nlog += nc;
+    prev = cnt;
     cnt = nc;
-    cur ^= 1;
+    cur = nxt;
+    if (phaseA ? found >= 0 : (lds32(snk_word) & snk_mask) != 0) break;
   }
-  __syncwarp();
+  C.arc_scans += arcs;
+  C.node_updates += upd;
+  C.add(kPrBfsLevels, levels);
+  int ret = found;
+  if (!phaseA) ret = (lds32(snk_word) & snk_mask) ? collect_ends(N, cur ^ 1, prev) : 0;
   C.add(kPrBfs, now() - t0);
-  return found;
+  return ret;
 }
 
-// Augments along the logged BFS path ending at log index `found` (node tgt):
-// lane 0 chases the parent links (one load per hop), then the warp updates
-// both sides of every path arc.  Phase A: amount = min(residuals, bal[src],
-// -bal[tgt]) and the balances move; phase B: amount = min(residuals), R grows.
-__device__ void augment(Net& N, int found, int tgt, bool phaseA, Counters& C) {
+// Pushes flow along a chain: position `first` (if >= 0), then the logged
+// parent links from log index `idx`, for at most `cap` units and, in phase A,
+// at most the excess bal[src] of the chain's source.  Lane 0 chases the
+// parent links only (one dependent load per hop); the warp then takes the
+// bottleneck over the chain's residuals in parallel and updates both sides
+// of every arc.  Returns the amount pushed (0 = chain blocked).
+__device__ long long push_chain(Net& N, int first, int idx, long long cap, bool phaseA, int& src,
+                                Counters& C) {
   const int ln = lane_id();
-  const long long t0 = now();
-  long long d = 0;
-  int k = 0, src = -1;
+  int k = 0, s = -1;
   if (ln == 0) {
-    d = phaseA ? -N.bal[tgt] : LLONG_MAX;
-    int idx = found;
+    if (first >= 0) N.path[k++] = first;
     for (;;) {
       const int2 l = N.lg[idx];
       if (l.x < 0) {
-        src = -1 - l.x;
+        s = -1 - l.x;
         break;
       }
-      const long long r = eff_res(N.resid[l.x], N.S);
-      d = r < d ? r : d;
       N.path[k++] = l.x;
       idx = l.y;
     }
-    if (phaseA) {
-      const long long b = N.bal[src];
-      d = b < d ? b : d;
-    }
   }
-  d = __shfl_sync(kFull, d, 0);
   k = __shfl_sync(kFull, k, 0);
-  src = __shfl_sync(kFull, src, 0);
+  src = __shfl_sync(kFull, s, 0);
   __syncwarp();
+  long long d = cap;
+  for (int q = ln; q < k; q += 32) {
+    const long long r = eff_res(N.resid[N.path[q]], N.S);
+    d = r < d ? r : d;
+  }
+  if (phaseA && ln == 0) {
+    const long long ex = N.bal[src];
+    d = ex < d ? ex : d;
+  }
+  d = wmin(d);
+  C.add(kPrPathHops, k);
+  if (ln == 0) C.node_updates += 2 * k;
+  if (d <= 0) return 0;
   for (int q = ln; q < k; q += 32) {
     const int p = N.path[q];
     N.resid[p] -= d;
     N.resid[N.ient[p].twin] += d;
   }
-  if (phaseA) {
-    if (ln == 0) {
-      N.bal[src] -= d;
-      N.bal[tgt] += d;
-    }
-  } else {
-    N.R += d;
-  }
-  C.add(kPrPaths, 1);
-  C.add(kPrPathHops, k);
-  if (ln == 0) C.node_updates += 2 * k;
   __syncwarp();
+  C.add(kPrPaths, 1);
+  return d;
+}
+
+// Phase A augmentation to the deficit node tgt (log index found): amount =
+// min(residuals, bal[src], -bal[tgt]); the balances move.
+__device__ void augment_a(Net& N, int found, int tgt, Counters& C) {
+  const long long t0 = now();
+  int src = -1;
+  const long long d = push_chain(N, -1, found, -N.bal[tgt], true, src, C);
+  if (d > 0 && lane_id() == 0) {
+    N.bal[src] -= d;
+    N.bal[tgt] += d;
+  }
+  __syncwarp();
+  C.add(kPrAugment, now() - t0);
+}
+
+// Phase B augmentation along every recorded end arc into the sink (paths of
+// one BFS level graph; each is re-checked against the current residuals).
+__device__ void augment_b(Net& N, int nend, Counters& C) {
+  const long long t0 = now();
+  for (int k = 0; k < nend; ++k) {
+    const int2 en = N.ends[k];
+    int src;
+    N.R += push_chain(N, en.x, en.y, LLONG_MAX, false, src, C);
+  }
   C.add(kPrAugment, now() - t0);
 }
 
@@ -323,7 +442,7 @@ __device__ bool repair(Net& N, int ntouch, Counters& C) {
       ok = false;
       break;
     }
-    augment(N, found, tgt, true, C);
+    augment_a(N, found, tgt, C);
   }
   __syncwarp();
   N.R = N.resid[N.ret_ph];
@@ -350,9 +469,9 @@ __device__ void maximize(Net& N, Counters& C) {
     __syncwarp();
     C.add(kPrBfsB, 1);
     int tgt;
-    const int found = bfs(N, 1, false, tgt, C);
-    if (found < 0) break;
-    augment(N, found, tgt, false, C);
+    const int nend = bfs(N, 1, false, tgt, C);
+    if (nend <= 0) break;
+    augment_b(N, nend, C);
   }
   C.add(kPrPhaseB, now() - t0);
 }
@@ -366,6 +485,7 @@ struct Walk {
   longlong2* tl;     // {planned duration + longest tail to the sink, 0}
   longlong2* cap;    // {lower, upper; -1 = infinite} of critical computation edges
   uint8_t* ecrit;    // [E] edge in the current critical network
+  uint8_t* dirty;    // [n] duration changed since the capacity was built
   uint8_t* choice;
   int32_t* delta;
 };
@@ -522,41 +642,103 @@ __device__ void write_point(const DevInst& I, int k, long long tp, long long tr,
 __device__ __forceinline__ int ec_tail_of(int n, int u) { return u == n ? 2 * n : 2 * u + 1; }
 __device__ __forceinline__ int ec_head_of(int n, int v) { return v == n + 1 ? 2 * n + 1 : 2 * v; }
 
-// K3: critical mask + Eq. 7 capacities + warm-start clamp for every edge.
-// Returns PB_OK or PB_ERR_OVERFLOW; ntouch = nodes whose balance moved.
-__device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, long long ms, int& ntouch,
-                          int* extrap, Counters& C) {
+// Curve value at t for a computation record: the host table inside
+// [t_min, t_max], the curve itself outside (counted, SURVEY.md §7 rule 5).
+__device__ __forceinline__ double table_rec(const DevInst& I, const CompRec& rc, int i, long long t,
+                                            int* extrap) {
+  if (t >= rc.tmin && t <= rc.tmax) return I.tables[rc.tab + (t - rc.tmin)];
+  return table_at(I, I.comp_class[i], t, extrap);
+}
+
+// Totals of the critical network (flow.hpp:58-68, 196-197), maintained
+// incrementally across the steps of a walk: sum of lower bounds, sum of
+// finite upper bounds, number of infinite edges.
+struct CapSums {
+  i128 suml, sumu;
+  long long ninf;
+};
+
+// K3: critical mask + Eq. 7 capacities + warm-start clamp.  Only "heavy"
+// edges are rebuilt: those whose criticality changed, and critical
+// computations whose duration (dirty) or the step size changed; every other
+// critical edge keeps its bounds and flow.  Returns PB_OK or
+// PB_ERR_OVERFLOW; ntouch = nodes whose balance moved.
+__device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, bool step_changed,
+                          long long ms, CapSums& T, int& ntouch, int* extrap, Counters& C) {
   const int ln = lane_id();
   const int n = I.n;
   const long long t0 = now();
   C.add(kPrSteps, 1);
-  i128 suml = 0, sumu = 0;
-  long long ninf = 0, max_inf_f = 0;
   ntouch = 0;
-  for (int base = 0; base < n; base += 32) {
-    const int i = base + ln;
+  i128 dl = 0, du = 0;
+  long long dinf = 0;
+  constexpr int kU = 4;
+  // stage 1: criticality of every computation, heavy ones compacted into W.delta
+  int nh = 0;
+  for (int base = 0; base < n; base += 32 * kU) {
+    long long t[kU], fx[kU], tx[kU];
+    bool oc[kU];
+    uint8_t dt[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int i = base + 32 * q + ln;
+      t[q] = fx[q] = tx[q] = 0;
+      oc[q] = false;
+      dt[q] = 0;
+      if (i < n) {
+        t[q] = W.durp[i];
+        fx[q] = W.fin[i].x;
+        tx[q] = W.tl[i].x;
+        oc[q] = W.ecrit[i];
+        dt[q] = W.dirty[i];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int i = base + 32 * q + ln;
+      bool heavy = false;
+      if (i < n) {
+        const bool crit = fx[q] + tx[q] - t[q] == ms;
+        heavy = crit != oc[q] || (crit && (dt[q] || step_changed));
+        if (dt[q]) W.dirty[i] = 0;
+      }
+      wappend(heavy, i, W.delta, nh);
+    }
+  }
+  __syncwarp();
+  // stage 2: heavy computations, one per lane
+  for (int base = 0; base < nh; base += 32) {
+    const int k = base + ln;
     bool ch = false;
-    if (i < n) {
-      const int c = I.comp_class[i];
+    int i = 0;
+    if (k < nh) {
+      i = W.delta[k];
       const long long t = W.durp[i];
       const bool crit = W.fin[i].x + W.tl[i].x - t == ms;
       const bool oc = W.ecrit[i];
-      const int2 ps = I.epos[i];
+      const CompRec rc = I.crec[i];
       long long fo = 0;
-      if (oc) fo = W.cap[i].x + N.resid[ps.y];
+      if (oc) {
+        const longlong2 cp = W.cap[i];
+        fo = cp.x + N.resid[rc.ph];
+        dl -= cp.x;
+        if (cp.y >= 0)
+          du -= cp.y;
+        else
+          --dinf;
+      }
       long long l = 0, u = 0;
       bool inf = true;
-      if (crit && !I.cls_const[c]) {
-        const long long tmin = I.cls_tmin[c], tmax = I.cls_tmax[c];
-        const bool can_speed = t - step >= tmin;
-        const bool can_slow = t + step <= tmax;
-        const double et = (can_speed || can_slow) ? table_at(I, c, t, extrap) : 0.0;
+      if (crit && rc.tab >= 0) {
+        const bool can_speed = t - step >= rc.tmin;
+        const bool can_slow = t + step <= rc.tmax;
+        const double et = (can_speed || can_slow) ? table_rec(I, rc, i, t, extrap) : 0.0;
         if (can_slow) {
-          const long long r = llround(et - table_at(I, c, t + step, extrap));
+          const long long r = llround(et - table_rec(I, rc, i, t + step, extrap));
           l = r > 0 ? r : 0;
         }
         if (can_speed) {
-          const long long r = llround(table_at(I, c, t - step, extrap) - et);
+          const long long r = llround(table_rec(I, rc, i, t - step, extrap) - et);
           u = r > l ? r : l;
           inf = false;
         }
@@ -565,20 +747,16 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, lon
       if (crit) {
         fn = fo < l ? l : fo;
         if (!inf && fn > u) fn = u;
-        suml += l;
-        if (!inf) {
-          sumu += u;
-        } else {
-          ++ninf;
-          max_inf_f = fn > max_inf_f ? fn : max_inf_f;
-        }
+        dl += l;
+        if (!inf)
+          du += u;
+        else
+          ++dinf;
       }
-      if (crit || oc) {
-        N.resid[ps.x] = crit ? (inf ? -(fn + 1) : u - fn) : 0;
-        N.resid[ps.y] = crit ? fn - l : 0;
-        W.cap[i] = make_longlong2(l, inf ? -1 : u);
-        W.ecrit[i] = crit;
-      }
+      N.resid[rc.pt] = crit ? (inf ? -(fn + 1) : u - fn) : 0;
+      N.resid[rc.ph] = crit ? fn - l : 0;
+      W.cap[i] = make_longlong2(l, inf ? -1 : u);
+      W.ecrit[i] = crit;
       if (fn != fo) {
         red_add(&N.bal[2 * i + 1], fn - fo);
         red_add(&N.bal[2 * i], fo - fn);
@@ -589,62 +767,84 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, lon
     wappend(ch, 2 * i + 1, N.touch, ntouch);
   }
   __syncwarp();
-  for (int base = 0; base < I.ne; base += 32) {
-    const int j = base + ln;
-    bool ch = false;
-    int et = 0, eh = 0;
-    if (j < I.ne) {
-      const int2 uv = I.dep_nd[j];
-      const int k = n + j;
-      bool tc = true, hc = true;
-      long long te = 0, he = ms;
-      if (uv.x != n) {
-        tc = W.ecrit[uv.x];
-        te = W.fin[uv.x].x;
-      }
-      if (uv.y != n + 1) {
-        hc = W.ecrit[uv.y];
-        he = W.fin[uv.y].x - W.durp[uv.y];
-      }
-      const bool crit = tc && hc && te == he;
-      const bool oc = W.ecrit[k];
-      const int2 ps = I.epos[k];
-      long long fo = 0;
-      if (oc) fo = N.resid[ps.y];
-      const long long fn = crit ? fo : 0;
-      if (crit || oc) {
-        N.resid[ps.y] = fn;
-        N.resid[ps.x] = crit ? -(fn + 1) : 0;
-        W.ecrit[k] = crit;
-      }
-      if (crit) {
-        ++ninf;
-        max_inf_f = fn > max_inf_f ? fn : max_inf_f;
-      }
-      if (fn != fo) {
-        et = ec_tail_of(n, uv.x);
-        eh = ec_head_of(n, uv.y);
-        red_add(&N.bal[eh], fn - fo);
-        red_add(&N.bal[et], fo - fn);
-        ch = true;
+  // dependency edges (always infinite, lower bound 0): only criticality changes matter
+  for (int base = 0; base < I.ne; base += 32 * kU) {
+    int2 uv[kU];
+    bool oc[kU], tc[kU], hc[kU];
+    long long te[kU], he[kU], hd[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int j = base + 32 * q + ln;
+      uv[q] = make_int2(n, n + 1);
+      oc[q] = false;
+      if (j < I.ne) {
+        uv[q] = I.dep_nd[j];
+        oc[q] = W.ecrit[n + j];
       }
     }
-    wappend(ch, et, N.touch, ntouch);
-    wappend(ch, eh, N.touch, ntouch);
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      tc[q] = hc[q] = true;
+      te[q] = 0;
+      he[q] = ms;
+      hd[q] = 0;
+      if (uv[q].x != n) {
+        tc[q] = W.ecrit[uv[q].x];
+        te[q] = W.fin[uv[q].x].x;
+      }
+      if (uv[q].y != n + 1) {
+        hc[q] = W.ecrit[uv[q].y];
+        he[q] = W.fin[uv[q].y].x;
+        hd[q] = W.durp[uv[q].y];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int j = base + 32 * q + ln;
+      bool ch = false;
+      int et = 0, eh = 0;
+      if (j < I.ne) {
+        const bool crit = tc[q] && hc[q] && te[q] == he[q] - hd[q];
+        if (crit != oc[q]) {
+          const int2 ps = I.epos[n + j];
+          W.ecrit[n + j] = crit;
+          if (crit) {
+            ++dinf;
+            N.resid[ps.y] = 0;
+            N.resid[ps.x] = -1;  // infinite forward side carrying f = 0
+          } else {
+            --dinf;
+            const long long fo = N.resid[ps.y];
+            N.resid[ps.y] = 0;
+            N.resid[ps.x] = 0;
+            if (fo != 0) {
+              et = ec_tail_of(n, uv[q].x);
+              eh = ec_head_of(n, uv[q].y);
+              red_add(&N.bal[eh], -fo);
+              red_add(&N.bal[et], fo);
+              ch = true;
+            }
+          }
+        }
+      }
+      wappend(ch, et, N.touch, ntouch);
+      wappend(ch, eh, N.touch, ntouch);
+    }
   }
-  suml = wsum128(suml);
-  sumu = wsum128(sumu);
-  ninf = wsum(ninf);
-  max_inf_f = wmax(max_inf_f);
+  T.suml += wsum128(dl);
+  T.sumu += wsum128(du);
+  T.ninf += wsum(dinf);
   // infinity_sentinel (flow.hpp:58-68) and the aux total (flow.hpp:196-197)
-  const i128 sent128 = suml + sumu + 1;
+  const i128 sent128 = T.suml + T.sumu + 1;
   if (sent128 > static_cast<i128>(LLONG_MAX / 4)) return PB_ERR_OVERFLOW;
   N.S = static_cast<long long>(sent128);
-  const i128 aux = sumu + static_cast<i128>(ninf) * N.S + suml;
+  const i128 aux = T.sumu + static_cast<i128>(T.ninf) * N.S + T.suml;
   if (aux + 1 > static_cast<i128>(LLONG_MAX / 2)) return PB_ERR_OVERFLOW;
   __syncwarp();
-  if (max_inf_f > N.S) {
-    // a carried flow exceeds the shrunken sentinel: clamp infinite edges
+  // The carried flow is an s-t flow of value R on a DAG, so no edge carries
+  // more than R: infinite edges need clamping only when R exceeds the new
+  // sentinel.
+  if (N.R > N.S) {
     const int nedges = n + I.ne;
     for (int base = 0; base < nedges; base += 32) {
       const int k = base + ln;
@@ -696,6 +896,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   for (int p = ln; p < 2 * I.E; p += 32) N.resid[p] = 0;
   for (int v = ln; v < I.V; v += 32) N.bal[v] = 0;
   for (int e = ln; e < I.E; e += 32) W.ecrit[e] = 0;
+  for (int i = ln; i < n; i += 32) W.dirty[i] = 0;
 
   int bad = 0;
   long long spe = 0, spt = 0, sre = 0, srt = 0;
@@ -735,7 +936,8 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   long long n_ids = 0;
   int status = PB_OK;
   int stop = PB_STOP_AT_TMIN;
-  const int nedges = n + I.ne;
+  long long prev_step = -1;
+  CapSums sums{0, 0, 0};
 
   for (;;) {
     long long step;
@@ -758,7 +960,9 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     }
     // ---- K3 critical network + capacities, carried flow clamped into the new bounds
     int ntouch = 0;
-    const int cs = build_caps(I, N, W, step, t_cur, ntouch, &bad, C);
+    const bool step_changed = step != prev_step;
+    prev_step = step;
+    const int cs = build_caps(I, N, W, step, step_changed, t_cur, sums, ntouch, &bad, C);
     if (cs != PB_OK) {
       status = cs;
       break;
@@ -773,41 +977,40 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       stop = PB_STOP_INFINITE_CUT;
       break;
     }
-    // ---- K5 minimal min cut = the last BFS's visited set
+    // ---- K5 minimal min cut = the last BFS's visited set.  A computation
+    // edge 2i -> 2i+1 crosses iff its two bits in the bitset word differ;
+    // its cost equals the max-flow value R (strong duality).
     const long long tupd = now();
-    long long cost = 0;
+    const long long cost = N.R;
     int nd = 0;
-    for (int base = 0; base < nedges; base += 32) {
-      const int k = base + ln;
-      int rec = 0;
-      if (k < nedges && W.ecrit[k]) {
-        int a, b;
-        if (k < n) {
-          a = 2 * k;
-          b = 2 * k + 1;
-        } else {
-          const int2 uv = I.dep_nd[k - n];
-          a = ec_tail_of(n, uv.x);
-          b = ec_head_of(n, uv.y);
-        }
-        const bool sa = bit_of(N, a), sb = bit_of(N, b);
-        if (sa && !sb) {
-          if (k < n) {
-            const long long u = W.cap[k].y;
-            cost += u < 0 ? N.S : u;
-            rec = k + 1;
-          } else {
-            cost += N.S;
-          }
-        } else if (!sa && sb && k < n) {
-          cost -= W.cap[k].x;
-          const int c = I.comp_class[k];
-          if (!I.cls_const[c] && W.durp[k] + step <= I.cls_tmax[c]) rec = -(k + 1);
-        }
+    const int ncw = (2 * n + 31) >> 5;
+    for (int base = 0; base < ncw; base += 32) {
+      const int w = base + ln;
+      uint32_t word = 0, x = 0;
+      if (w < ncw) {
+        word = lds32(N.s_bits + 4u * w);
+        x = (word ^ (word >> 1)) & 0x55555555u;
+        const int lim = 2 * n - 32 * w;  // bits from lim on are the source / sink
+        if (lim < 32) x &= (1u << lim) - 1u;
       }
-      wappend(rec != 0, rec, W.delta, nd);
+      while (__ballot_sync(kFull, x != 0)) {
+        int rec = 0;
+        if (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1;
+          const int i = (32 * w + b) >> 1;
+          if (W.ecrit[i]) {
+            if ((word >> b) & 1u) {
+              rec = i + 1;  // start in S, end in T: speed up
+            } else {
+              const CompRec rc = I.crec[i];  // T -> S: slow down (frontier.hpp:117-125)
+              if (rc.tab >= 0 && W.durp[i] + step <= rc.tmax) rec = -(i + 1);
+            }
+          }
+        }
+        wappend(rec != 0, rec, W.delta, nd);
+      }
     }
-    cost = wsum(cost);
     __syncwarp();
     // reserve a contiguous range of the batch delta pool
     unsigned long long at = 0;
@@ -858,6 +1061,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       const int ch = discretize_choice(I, c, tnew);
       W.choice[i] = static_cast<uint8_t>(ch);
       W.durr[i] = I.pt_time[I.cls_pt_off[c] + ch];
+      W.dirty[i] = 1;
     }
     __syncwarp();
     const int ns = static_cast<int>(wsum(ns_loc));
@@ -923,11 +1127,14 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.W.tl = reinterpret_cast<longlong2*>(base + L.off_hl);
   p.W.cap = reinterpret_cast<longlong2*>(base + L.off_cap);
   p.W.ecrit = reinterpret_cast<uint8_t*>(base + L.off_ecrit);
+  p.W.dirty = reinterpret_cast<uint8_t*>(base + L.off_ccrit);
   p.W.choice = reinterpret_cast<uint8_t*>(base + L.off_choice);
   p.W.delta = reinterpret_cast<int32_t*>(base + L.off_delta);
-  // shared memory: frontier (16 B aligned) then bitset
-  p.N.fs = reinterpret_cast<int4*>(smem);
-  p.N.bits = reinterpret_cast<uint32_t*>(smem + 16 * 2 * kFrontCap);
+  // shared memory: path ends, frontier (16 B aligned), bitset
+  p.N.ends = reinterpret_cast<int2*>(smem);
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  p.N.s_fs = sa + 8 * kMaxEnds;
+  p.N.s_bits = sa + 8 * kMaxEnds + 16 * 2 * kFrontCap;
   return p;
 }
 
@@ -952,7 +1159,7 @@ __device__ __forceinline__ int warp_slot() { return blockIdx.x * kWarpsPerBlock 
 extern __shared__ __align__(16) char g_smem[];
 
 __device__ __forceinline__ char* my_smem(const WsLayout& L, unsigned long long** prof) {
-  const int per = 128 + L.smem_bytes;
+  const int per = 128 + 8 * kMaxEnds + L.smem_bytes;
   char* base = g_smem + warp_in_block() * per;
   *prof = reinterpret_cast<unsigned long long*>(base);
   if (lane_id() < kPrSlots) (*prof)[lane_id()] = 0;
@@ -960,7 +1167,7 @@ __device__ __forceinline__ char* my_smem(const WsLayout& L, unsigned long long**
   return base + 128;
 }
 
-__global__ void __launch_bounds__(kBlock) walk_kernel(const DevInst* insts, int n_inst,
+__global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel(const DevInst* insts, int n_inst,
                                                       const int32_t* order, int32_t* counter,
                                                       char* ws_base, WsLayout L, int slots,
                                                       RunCounters* ctr, DeltaPool pool) {
@@ -1164,7 +1371,9 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
 }
 
 int blocks_for(int slots) { return (slots + kWarpsPerBlock - 1) / kWarpsPerBlock; }
-size_t block_smem(const WsLayout& L) { return static_cast<size_t>(kWarpsPerBlock) * (128 + L.smem_bytes); }
+size_t block_smem(const WsLayout& L) {
+  return static_cast<size_t>(kWarpsPerBlock) * (128 + 8 * kMaxEnds + L.smem_bytes);
+}
 
 template <class K>
 void set_smem(K kernel, size_t bytes) {

@@ -1,6 +1,6 @@
 """Per-phase device profile of the frontier-walk kernel (pb_batch_profile).
 
-  python tools/walk_profile.py config2 [config4 ...] [batch:N]
+  python tools/walk_profile.py config2 [config4 ...] [config1*1776] [batch:N]
 """
 import ctypes as C
 import os
@@ -20,7 +20,9 @@ NAMES = ["lp", "cap", "phaseA", "phaseB", "bfs", "augment", "update", "walk", "b
 def profile(name):
     b = pb.FrontierBatch()
     if name.startswith("config"):
-        b.add_g9(g9.named_config(int(name[-1])))
+        k, _, reps = name[len("config"):].partition("*")
+        for _ in range(int(reps or 1)):
+            b.add_g9(g9.named_config(int(k)))
     elif name.startswith("batch:"):
         for i in range(int(name.split(":")[1])):
             b.add_g9(g9.batch_params(i))
