@@ -233,6 +233,15 @@ def build_batch_specs(args):
     return None, f"G9 config {k}", [f"config:{k}"] * max(1, args.reps), None
 
 
+def load_traffic():
+    """dram read+write bytes per launch of the walk kernel from the committed
+    ncu --set full capture of the default workload (profiles/), if any."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "walk_traffic.json")))
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -284,31 +293,38 @@ def run_ours(args):
     st_e2e = b.stats()
     t_e2e = D.max(sum(e2e_times))
     e2e_value = total_points * len(e2e_times) / t_e2e
-    # roofline of the walk kernel: algorithmic bytes from the device counters
-    # (16 B per arc scan, 24 B per node update, 24 B per longest-path visit;
-    # SURVEY.md §8d) over the measured launch time
-    alg_bytes = 16 * st.arc_scans + 24 * st.node_updates + 24 * st.comp_visits
+    # roofline of the walk kernel: algorithmic bytes
+    # from the device work counters over the device-timed launch duration.
+    #   arc scan          24 B  (16 B incidence entry + 8 B residual)
+    #   node update       16 B  (8 B BFS-log entry + 8 B residual side on augment)
+    #   longest-path visit 48 B (16 B row record + 16 B predecessor value + 16 B store)
+    alg_bytes = 24 * st.arc_scans + 16 * st.node_updates + 48 * st.comp_visits
     launch_s = st.kernel_ms / 1e3
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = alg_bytes / launch_s / 1e9 if launch_s > 0 else 0.0
+    traffic = load_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (G9 generator, SURVEY.md §8d)",
         "config": {"workload": desc, "instances_per_rank": len(b), "tau_us": 1000,
-                   "l2": "working set > 126 MB L2 (instance data + per-CTA residual state); no flush",
-                   "parallelism": f"instances sharded over {world} GPU(s), one CTA per instance"},
+                   "l2": "no flush: per-walker workspaces + instance data exceed the 126 MB L2",
+                   "parallelism": f"instances sharded over {world} GPU(s), one warp per instance"},
         "iterations_per_s": total_steps * args.steps / t_dev,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(st_e2e.h2d_bytes),
                 "d2h_bytes_per_step": int(st_e2e.d2h_bytes)},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None,
+                     "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                     "traffic_source": traffic.get("source") if traffic else None,
+                     "algorithmic_bytes_per_launch": alg_bytes,
                      "counters": {"arc_scans": st.arc_scans, "node_updates": st.node_updates,
-                                  "comp_visits": st.comp_visits, "rounds": st.rounds},
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+                                  "comp_visits": st.comp_visits, "bfs_levels": st.rounds},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks
+                     else "fallback 6650 GB/s"},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu and os.path.exists(ref_driver_path()):
@@ -333,7 +349,8 @@ def main():
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-steps", type=int, default=1)
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0,
+                    help="seconds per sampled instance for the reference CPU planner")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

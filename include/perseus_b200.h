@@ -106,7 +106,8 @@ typedef struct {
    * of the host table; the reference evaluates the curve there too,
    * costmodel.hpp:47).  0 on every G9 and golden walk. */
   int32_t n_extrapolated;
-  int32_t pad;
+  /* device time of this walk (microseconds, %globaltimer); diagnostics */
+  int32_t walk_us;
 } pb_frontier_summary;
 
 /* Per-point scalars; point 0 is the T* seed, point k>0 follows step k. */

@@ -94,7 +94,7 @@ class FrontierSummary(C.Structure):
         ("status", C.c_int32),
         ("n_ids", C.c_int32),
         ("n_extrapolated", C.c_int32),
-        ("pad", C.c_int32),
+        ("walk_us", C.c_int32),
     ]
 
 

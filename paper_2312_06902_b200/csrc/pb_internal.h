@@ -125,7 +125,7 @@ enum : int {
 };
 
 // Shared memory per walker warp: visited bitset + ping-pong frontier.
-constexpr int kFrontCap = 64;  // frontier entries per buffer kept in smem
+constexpr int kFrontCap = 128;  // frontier entries per buffer kept in smem
 
 // Per-warp global workspace; arrays sized for the largest instance of a batch.
 // The flow (encoded in resid) persists across the steps of a walk.

@@ -99,6 +99,11 @@ __device__ __forceinline__ void red_add(long long* p, long long d) {
 }
 
 __device__ __forceinline__ long long now() { return clock64(); }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Work counters: per-lane in registers (flushed once per warp), phase
 // profile in shared memory (lane 0 only).
@@ -191,32 +196,6 @@ __device__ __forceinline__ void seed(Net& N, int k, int v) {
   N.lg[k] = make_int2(-1 - v, -1);
 }
 
-// One BFS discovery: ballot-compacts the lanes whose arc p (from the
-// frontier entry with log index parent) discovered node e.other.
-__device__ __forceinline__ void discover(Net& N, bool c, int p, const IEnt& e, int parent, int nlog, int nxt,
-                                         int& nc, bool phaseA, int& found, int& tgt, unsigned& upd) {
-  const unsigned m = __ballot_sync(kFull, c);
-  if (!m) return;
-  const int pos = nc + __popc(m & lanemask_lt());
-  bool hit = false;
-  if (c) {
-    const int li = nlog + pos;
-    N.lg[li] = make_int2(p, parent);
-    fwrite(N, nxt, pos, make_int4(e.other, e.other_off, e.other_end, li));
-    if (phaseA) hit = N.bal[e.other] < 0;
-    ++upd;
-  }
-  if (phaseA) {
-    const unsigned h = __ballot_sync(kFull, hit);
-    if (h && found < 0) {
-      const int hl = __ffs(h) - 1;
-      found = __shfl_sync(kFull, nlog + pos, hl);
-      tgt = __shfl_sync(kFull, e.other, hl);
-    }
-  }
-  nc += __popc(m);
-}
-
 // Phase B: the arcs of frontier buffer buf (cnt entries) that enter the sink
 // with positive residual -> N.ends (at most kMaxEnds).
 __device__ int collect_ends(Net& N, int buf, int cnt) {
@@ -246,16 +225,19 @@ __device__ int collect_ends(Net& N, int buf, int cnt) {
 }
 
 // Level-synchronous BFS over residual arcs from the nsrc seeded sources
-// (already marked).  A lane owns 2 arcs of a round and issues both
-// {ient, resid} loads before using either; the bitset test-and-set is an
-// unconditional shared atomic (mask 0 for non-arcs).  phaseA: targets are
-// nodes with bal < 0; stops after the level that reaches one and returns
-// its log index (tgt = node).  Phase B: stops after the level that marks
-// the sink (one shared load per level) and returns the number of that
-// level's arcs into the sink, recorded in N.ends (0 = sink unreachable; the
-// bitset then marks exactly the residual-reachable set).  -1: nothing found.
-__device__ int bfs(Net& N, int nsrc, bool phaseA, int& tgt, Counters& C) {
+// (already marked).  g = 1, 2 or 4 lanes share a frontier node and take its
+// arcs round-robin; per arc one {ient, resid} load pair, one unconditional
+// shared atomic test-and-set (mask 0 for non-arcs) and one ballot.  The
+// frontier lives in shared memory (spilling to global past kFrontCap).
+// Phase A (kA): targets are nodes with bal < 0; stops after the level that
+// reaches one and returns its log index (tgt = node).  Phase B: stops after
+// the level that marks the sink (one shared load per level) and returns the
+// number of that level's arcs into the sink, recorded in N.ends (0 = sink
+// unreachable; the bitset then marks exactly the residual-reachable set).
+template <bool kA>
+__device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
   const int ln = lane_id();
+  const unsigned lt = lanemask_lt();
   const long long t0 = now();
   const long long negS = -N.S;  // raw residual r is positive iff r != 0 && r >= -S
   int cnt = nsrc, cur = 0, nlog = nsrc, found = -1, levels = 0, prev = 0;
@@ -264,38 +246,57 @@ __device__ int bfs(Net& N, int nsrc, bool phaseA, int& tgt, Counters& C) {
   const uint32_t snk_word = N.s_bits + 4u * (N.snk >> 5), snk_mask = 1u << (N.snk & 31);
   while (cnt > 0) {
     ++levels;
-    const int lg2 = cnt >= 16 ? 0 : cnt >= 8 ? 1 : cnt >= 4 ? 2 : 3;  // lanes per frontier node
+    const int lg2 = cnt <= 8 ? 2 : (cnt <= 16 ? 1 : 0);
     const int g = 1 << lg2;
     const int sub = ln & (g - 1);
     const int nxt = cur ^ 1;
+    const uint32_t fcur = N.s_fs + 16u * kFrontCap * cur, fnxt = N.s_fs + 16u * kFrontCap * nxt;
+    int4* gcur = N.fglob + static_cast<size_t>(cur) * N.fstride;
+    int4* gnxt = N.fglob + static_cast<size_t>(nxt) * N.fstride;
     int nc = 0;
     for (int base = 0; base < cnt; base += 32 >> lg2) {
       const int slot = base + (ln >> lg2);
       int4 fe = make_int4(0, 0, 0, 0);
-      if (slot < cnt) fe = fread(N, cur, slot);
-      const int deg = fe.z - fe.y;
-      const int myr = deg > sub ? (deg - sub + g - 1) >> lg2 : 0;
-      const int rounds = wmaxi(myr);
-      arcs += myr;
-      for (int r = 0; r < rounds; r += 2) {
-        const int p0 = fe.y + sub + (r << lg2), p1 = p0 + g;
-        IEnt e0{0, 0, 0, 0}, e1{0, 0, 0, 0};
-        long long w0 = 0, w1 = 0;
-        if (r < myr) {
-          e0 = N.ient[p0];
-          w0 = N.resid[p0];
+      if (slot < cnt) fe = slot < kFrontCap ? lds128(fcur + 16u * slot) : gcur[slot];
+      int p = fe.y + sub;
+      const int mine = fe.z > p ? (fe.z - p + g - 1) >> lg2 : 0;
+      const int rounds = wmaxi(mine);
+      arcs += mine;
+      for (int r = 0; r < rounds; ++r, p += g) {
+        const bool v = p < fe.z;
+        IEnt e{0, 0, 0, 0};
+        long long w = 0;
+        if (v) {
+          e = N.ient[p];
+          w = N.resid[p];
         }
-        if (r + 1 < myr) {
-          e1 = N.ient[p1];
-          w1 = N.resid[p1];
+        const bool ok = w != 0 && w >= negS;
+        const uint32_t m = ok ? 1u << (e.other & 31) : 0u;
+        const uint32_t o = atoms_or(N.s_bits + 4u * (e.other >> 5), m);
+        const bool c = ok && (o & m) == 0;
+        const unsigned bm = __ballot_sync(kFull, c);
+        const int pos = nc + __popc(bm & lt);
+        bool hit = false;
+        if (c) {
+          const int li = nlog + pos;
+          N.lg[li] = make_int2(p, fe.w);
+          const int4 ent = make_int4(e.other, e.other_off, e.other_end, li);
+          if (pos < kFrontCap)
+            sts128(fnxt + 16u * pos, ent);
+          else
+            gnxt[pos] = ent;
+          if (kA) hit = N.bal[e.other] < 0;
         }
-        const bool ok0 = w0 != 0 && w0 >= negS, ok1 = w1 != 0 && w1 >= negS;
-        const uint32_t m0 = ok0 ? 1u << (e0.other & 31) : 0u;
-        const uint32_t o0 = atoms_or(N.s_bits + 4u * (e0.other >> 5), m0);
-        const uint32_t m1 = ok1 ? 1u << (e1.other & 31) : 0u;
-        const uint32_t o1 = atoms_or(N.s_bits + 4u * (e1.other >> 5), m1);
-        discover(N, ok0 && !(o0 & m0), p0, e0, fe.w, nlog, nxt, nc, phaseA, found, tgt, upd);
-        if (r + 1 < rounds) discover(N, ok1 && !(o1 & m1), p1, e1, fe.w, nlog, nxt, nc, phaseA, found, tgt, upd);
+        if (kA) {
+          const unsigned h = __ballot_sync(kFull, hit);
+          if (h && found < 0) {
+            const int hl = __ffs(h) - 1;
+            found = __shfl_sync(kFull, nlog + pos, hl);
+            tgt = __shfl_sync(kFull, e.other, hl);
+          }
+        }
+        nc += __popc(bm);
+        upd += c;
       }
     }
     __syncwarp();
@@ -303,13 +304,13 @@ __device__ int bfs(Net& N, int nsrc, bool phaseA, int& tgt, Counters& C) {
     prev = cnt;
     cnt = nc;
     cur = nxt;
-    if (phaseA ? found >= 0 : (lds32(snk_word) & snk_mask) != 0) break;
+    if (kA ? found >= 0 : (lds32(snk_word) & snk_mask) != 0) break;
   }
   C.arc_scans += arcs;
   C.node_updates += upd;
   C.add(kPrBfsLevels, levels);
   int ret = found;
-  if (!phaseA) ret = (lds32(snk_word) & snk_mask) ? collect_ends(N, cur ^ 1, prev) : 0;
+  if (!kA) ret = (lds32(snk_word) & snk_mask) ? collect_ends(N, cur ^ 1, prev) : 0;
   C.add(kPrBfs, now() - t0);
   return ret;
 }
@@ -437,7 +438,7 @@ __device__ bool repair(Net& N, int ntouch, Counters& C) {
     nex = ns;
     C.add(kPrBfsA, 1);
     int tgt;
-    const int found = bfs(N, ns, true, tgt, C);
+    const int found = bfs<true>(N, ns, tgt, C);
     if (found < 0) {
       ok = false;
       break;
@@ -469,7 +470,7 @@ __device__ void maximize(Net& N, Counters& C) {
     __syncwarp();
     C.add(kPrBfsB, 1);
     int tgt;
-    const int nend = bfs(N, 1, false, tgt, C);
+    const int nend = bfs<false>(N, 1, tgt, C);
     if (nend <= 0) break;
     augment_b(N, nend, C);
   }
@@ -882,6 +883,7 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
 
 __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& pool, Counters& C) {
   const int ln = lane_id();
+  const unsigned long long g0 = gtimer();
   const int n = I.n;
   N.V = I.V;
   N.src = 2 * n;
@@ -1100,7 +1102,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     s.status = status;
     s.n_ids = static_cast<int32_t>(n_ids);
     s.n_extrapolated = static_cast<int32_t>(n_extrap);
-    s.pad = 0;
+    s.walk_us = static_cast<int32_t>((gtimer() - g0) / 1000);
     *I.summary = s;
   }
   __syncwarp();

@@ -34,7 +34,7 @@ def profile(name):
     N.check(N.lib.pb_batch_profile(b._h, N.ptr(prof, C.c_int64), 16))
     st = b.stats()
     steps = sum(b.summary(k).steps for k in range(len(b)))
-    bad = [(k, b.summary(k).status, b.summary(k).pad, b.summary(k).steps) for k in range(len(b)) if b.summary(k).status]
+    bad = [(k, b.summary(k).status, b.summary(k).n_extrapolated, b.summary(k).steps) for k in range(len(b)) if b.summary(k).status]
     walk = max(prof[7], 1)
     print(f"== {name}: kernel {ms:.1f} ms, {steps} steps, {ms * 1e3 / max(steps, 1):.1f} us/step, wall {time.time() - t:.1f}s")
     print("   cycles share: " + ", ".join(f"{NAMES[i]} {prof[i] / walk:.1%}" for i in range(7)))
@@ -42,6 +42,16 @@ def profile(name):
     print("   per step: " + ", ".join(f"{NAMES[i]} {prof[i] / S:.2f}" for i in range(8, 16)))
     print(f"   cycles/step {prof[7] / S:.0f}, cycles per bfs level {prof[4] / max(prof[10], 1):.0f}")
     print(f"   arc_scans/step {st.arc_scans / S:.0f}, node_updates/step {st.node_updates / S:.0f}")
+    walks = sorted(((b.summary(k).walk_us, k) for k in range(len(b))), reverse=True)
+    if len(walks) > 1:
+        import heapq
+        slots = [0.0] * min(len(walks), int(os.environ.get("PB_SLOTS", "1776")))
+        heapq.heapify(slots)
+        for us, _ in walks:  # LPT order approximates the device's queue order
+            t = heapq.heappop(slots)
+            heapq.heappush(slots, t + us)
+        print(f"   walks: longest {walks[0][0] / 1e3:.1f} ms, median {walks[len(walks) // 2][0] / 1e3:.2f} ms, "
+              f"sum {sum(w for w, _ in walks) / 1e6:.1f} s; LPT replay makespan {max(slots) / 1e3:.1f} ms")
     if bad:
         print("   FAILED (index, status, detail, steps):", bad[:10])
 
