@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -85,8 +86,9 @@ namespace pb {
 // per node the list of its arcs; entry p = {other end, twin position,
 // other's list range}; epos[k] = {position at tail, position at head}.
 void build_net(int32_t V, const std::vector<int32_t>& tail, const std::vector<int32_t>& head,
-               NetLayout& out) {
+               NetLayout& out, int32_t pairs) {
   const int32_t E = static_cast<int32_t>(tail.size());
+  if (2 * static_cast<int64_t>(E) > kTwinMask) throw std::length_error("flow network too large for 26-bit positions");
   out.inc_off.assign(V + 1, 0);
   for (int32_t k = 0; k < E; ++k) {
     ++out.inc_off[tail[k] + 1];
@@ -94,16 +96,24 @@ void build_net(int32_t V, const std::vector<int32_t>& tail, const std::vector<in
   }
   for (int32_t v = 0; v < V; ++v) out.inc_off[v + 1] += out.inc_off[v];
   out.epos.assign(E, int2h{0, 0});
+  // edges are placed in index order, so computation edge i (< pairs) is the
+  // first entry of both nodes 2i and 2i+1
   std::vector<int32_t> fill(out.inc_off.begin(), out.inc_off.end() - 1);
   for (int32_t k = 0; k < E; ++k) {
     out.epos[k].x = fill[tail[k]]++;
     out.epos[k].y = fill[head[k]]++;
   }
+  auto pdeg = [&](int32_t b) {
+    if (b >= 2 * pairs) return kNoPartner;
+    const int32_t d = out.inc_off[(b ^ 1) + 1] - out.inc_off[b ^ 1];
+    return d < kNoPartner ? d : kNoPartner;
+  };
   out.ient.assign(out.inc_off[V], IEnt{0, 0, 0, 0});
   for (int32_t k = 0; k < E; ++k) {
     const int32_t a = tail[k], b = head[k], pa = out.epos[k].x, pb = out.epos[k].y;
-    out.ient[pa] = IEnt{b, pb, out.inc_off[b], out.inc_off[b + 1]};
-    out.ient[pb] = IEnt{a, pa, out.inc_off[a], out.inc_off[a + 1]};
+    const int32_t flag = k < pairs ? kCompArc : 0;
+    out.ient[pa] = IEnt{b, pb | flag | (pdeg(b) << kPdegShift), out.inc_off[b], out.inc_off[b + 1]};
+    out.ient[pb] = IEnt{a, pa | flag | (pdeg(a) << kPdegShift), out.inc_off[a], out.inc_off[a + 1]};
   }
 }
 }  // namespace pb
@@ -227,7 +237,7 @@ pb_status validate_and_derive(HostInst& h) {
   }
   et[n + ne] = 2 * n + 1;
   eh[n + ne] = 2 * n;
-  pb::build_net(V, et, eh, h.net);
+  pb::build_net(V, et, eh, h.net, n);
   if (!h.start.empty()) {
     h.istart.assign(n, 0);
     for (int32_t i = 0; i < n; ++i) h.istart[h.inv[i]] = h.start[i];
@@ -302,8 +312,9 @@ struct DeviceRun {
   size_t out_bytes = 0;
   int32_t slots = 0;
   pb::WsLayout ws{};
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t stream = nullptr, stream_big = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_big = nullptr;
+  int32_t n_big = 0;
   char* h_out = nullptr;  // pinned
   void release() {
     if (device < 0) return;
@@ -321,7 +332,9 @@ struct DeviceRun {
     if (h_out) cudaFreeHost(h_out);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_big) cudaEventDestroy(ev_big);
     if (stream) cudaStreamDestroy(stream);
+    if (stream_big) cudaStreamDestroy(stream_big);
     *this = DeviceRun{};
   }
 };
@@ -543,11 +556,34 @@ void bind_device(Packed& P, char* d_static, char* d_out, size_t tables_off) {
   }
 }
 
-int32_t device_slots(int device, int64_t n_inst, const pb::WsLayout& ws) {
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
+// Exclusive-SM walks (pb_internal.h launch_walks): the LPT head whose
+// estimated work is within PB_BIG_FRAC (default 0.9) of the largest, at most
+// a quarter of the SMs, and only for batches that fill the device.
+// PB_BIG overrides the count.
+int32_t choose_big(const pb_batch* b, const std::vector<int32_t>& order, int sms, int per_sm) {
+  const int64_t N = static_cast<int64_t>(order.size());
+  int big = env_int("PB_BIG", 0);  // measured: no gain, off by default
+  if (big < 0) {
+    big = 0;
+    if (N > int64_t{sms} * per_sm / 2 && N > 0) {
+      const double frac = env_int("PB_BIG_PERMILLE", 900) / 1000.0;
+      const double top = static_cast<double>(b->insts[order[0]].work);
+      while (big < sms / 4 && big < N && static_cast<double>(b->insts[order[big]].work) >= frac * top) ++big;
+    }
+  }
+  return static_cast<int32_t>(std::min<int64_t>({int64_t{big}, N, int64_t{sms}}));
+}
+
+int32_t device_slots(int device, int64_t n_walk, const pb::WsLayout& ws, int32_t n_big) {
   int sms = 0;
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
-  const int per_sm = std::max(1, pb::walk_slots_per_sm(ws));
-  return static_cast<int32_t>(std::min<int64_t>(n_inst, int64_t{sms} * per_sm));
+  const int per_sm = std::max(1, env_int("PB_WARPS_PER_SM", pb::walk_slots_per_sm(ws)));
+  return static_cast<int32_t>(std::min<int64_t>(n_walk, int64_t{sms - n_big} * per_sm));
 }
 
 pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
@@ -563,6 +599,8 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   pack(b, P, capp, cap_scale);
   const size_t tables_off = 0;  // tables are the first section of the blob
   ck(cudaStreamCreateWithFlags(&R.stream, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&R.stream_big, cudaStreamNonBlocking), "stream");
+  ck(cudaEventCreateWithFlags(&R.ev_big, cudaEventDisableTiming), "event");
   ck(cudaEventCreate(&R.ev0), "event");
   ck(cudaEventCreate(&R.ev1), "event");
   cudaEvent_t h0, h1;
@@ -574,11 +612,16 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   ck(cudaMallocHost(&R.h_out, R.out_bytes), "malloc pinned out");
   bind_device(P, R.d_static, R.d_out, tables_off);
   R.ws = pb::make_ws_layout(P.max_n, P.max_v, P.max_e);
-  R.slots = device_slots(device, static_cast<int64_t>(N), R.ws);
-  ck(cudaMalloc(&R.d_ws, static_cast<size_t>(R.ws.stride) * R.slots), "malloc workspace");
+  {
+    int sms = 0;
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+    R.n_big = choose_big(b, P.order, sms, std::max(1, pb::walk_slots_per_sm(R.ws)));
+  }
+  R.slots = device_slots(device, static_cast<int64_t>(N) - R.n_big, R.ws, R.n_big);
+  ck(cudaMalloc(&R.d_ws, static_cast<size_t>(R.ws.stride) * (R.slots + R.n_big)), "malloc workspace");
   ck(cudaMalloc(&R.d_insts, sizeof(pb::DevInst) * N), "malloc insts");
   ck(cudaMalloc(&R.d_order, sizeof(int32_t) * N), "malloc order");
-  ck(cudaMalloc(&R.d_counter, sizeof(int32_t)), "malloc counter");
+  ck(cudaMalloc(&R.d_counter, 2 * sizeof(int32_t)), "malloc counter");
   ck(cudaMalloc(&R.d_counters, sizeof(pb::RunCounters)), "malloc counters");
   R.pool_cap = P.pool_cap;
   ck(cudaMalloc(&R.d_pool_ids, sizeof(int32_t) * std::max<long long>(R.pool_cap, 1)), "malloc pool");
@@ -616,14 +659,18 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   }
   if (R.device < 0) return fail(PB_ERR_LOGIC, "batch not prepared");
   ck(cudaSetDevice(R.device), "cudaSetDevice");
-  ck(cudaMemsetAsync(R.d_counter, 0, sizeof(int32_t), R.stream), "memset");
+  ck(cudaMemsetAsync(R.d_counter, 0, 2 * sizeof(int32_t), R.stream), "memset");
   ck(cudaMemsetAsync(R.d_counters, 0, sizeof(pb::RunCounters), R.stream), "memset");
   ck(cudaMemsetAsync(R.d_pool_cursor, 0, sizeof(unsigned long long), R.stream), "memset");
   pb::DeltaPool pool{R.d_pool_ids, R.d_pool_choice, R.d_pool_cursor, R.pool_cap};
   ck(cudaEventRecord(R.ev0, R.stream), "record");
+  ck(cudaStreamWaitEvent(R.stream_big, R.ev0, 0), "wait");
   const int rc = pb::launch_walks(R.d_insts, static_cast<int32_t>(N), R.d_order, R.d_counter,
-                                  R.d_ws, R.ws, R.slots, R.d_counters, pool, R.stream);
+                                  R.d_ws, R.ws, R.slots, R.d_counters, pool, R.n_big, R.stream,
+                                  R.stream_big);
   if (rc != 0) throw CudaError(std::string("walk launch: ") + cudaGetErrorString(static_cast<cudaError_t>(rc)));
+  ck(cudaEventRecord(R.ev_big, R.stream_big), "record");
+  ck(cudaStreamWaitEvent(R.stream, R.ev_big, 0), "wait");
   ck(cudaEventRecord(R.ev1, R.stream), "record");
   ck(cudaStreamSynchronize(R.stream), "walk kernel");
   float ms = 0;
@@ -636,7 +683,7 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   b->stats.rounds = static_cast<int64_t>(rcnt.rounds);
   b->stats.comp_visits = static_cast<int64_t>(rcnt.comp_visits);
   for (int q = 0; q < pb::kPrSlots; ++q) b->prof[q] = static_cast<int64_t>(rcnt.prof[q]);
-  b->stats.kernel_launches += 1;
+  b->stats.kernel_launches += (R.n_big > 0 ? 1 : 0) + (static_cast<int32_t>(N) > R.n_big ? 1 : 0);
   if (kernel_ms) *kernel_ms = ms;
   return PB_OK;
 }

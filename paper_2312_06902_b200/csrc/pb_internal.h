@@ -26,12 +26,20 @@ enum : int32_t { kModeDiscover = 0, kModeGetNext = 1 };
 enum : int32_t { kStatusLogFull = 100 };
 
 // Incidence entry (16 B, one LDG.128): the arc leaving the owning node.
-struct IEnt {
+// `twin` packs the position of the same edge in other's list (bits 0-25),
+// a computation-arc flag (bit 26) and the degree of other's partner node
+// other ^ 1 (bits 27-31; kNoPartner = no shortcut).  Computation arcs are
+// the FIRST entry of both of their nodes' lists.
+struct alignas(16) IEnt {
   int32_t other;      // node at the other end
-  int32_t twin;       // position of the same edge in other's list
+  int32_t twin;       // packed, see above
   int32_t other_off;  // other's list = [other_off, other_end)
   int32_t other_end;
 };
+constexpr int32_t kTwinMask = (1 << 26) - 1;
+constexpr int32_t kCompArc = 1 << 26;
+constexpr int kPdegShift = 27;
+constexpr int kNoPartner = 31;
 
 // Per-computation static record for the capacity build (32 B): the class's
 // curve interval, its table offset (tab < 0: constant class) and the
@@ -55,8 +63,10 @@ struct NetLayout {
   std::vector<IEnt> ient;
   std::vector<int2h> epos;
 };
+// pairs = n for an edge-centric walk network (nodes 2i, 2i+1 joined by
+// computation edge i, i < n), 0 for a generic flow graph (no shortcut).
 void build_net(int32_t V, const std::vector<int32_t>& tail, const std::vector<int32_t>& head,
-               NetLayout& out);
+               NetLayout& out, int32_t pairs = 0);
 
 // One packed instance: every pointer is a DEVICE address into the batch blob
 // (static data) or the output blob.
@@ -185,7 +195,8 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   L.off_path = take(4 * max_v);
   L.stride = o;
   const int64_t bitwords = (max_v + 31) / 32;
-  L.smem_bytes = static_cast<int32_t>(align_up(4 * bitwords, 16) + 16 * 2 * kFrontCap);
+  // frontier, visited bitset, partner-ok bitset
+  L.smem_bytes = static_cast<int32_t>(16 * 2 * kFrontCap + 2 * align_up(4 * bitwords, 16));
   return L;
 }
 
@@ -222,9 +233,15 @@ struct SlackOut {
 
 // Host-side launchers (pb_kernels.cu).  slots = number of walker warps (one
 // workspace each).
+// The first n_big instances of the LPT order run in a separate launch of
+// one-warp CTAs that claim a whole SM's shared memory each (exclusive SMs:
+// the longest walks bound the batch and must not share an SM); the rest run
+// in the persistent walker kernel (`slots` warps) on the remaining SMs.
+// Workspace slots: [0, n_big) big walks, [n_big, n_big + slots) walkers.
 int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
                  char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
-                 DeltaPool pool, void* stream);
+                 DeltaPool pool, int32_t n_big, void* stream, void* stream_big);
+int big_walk_smem_bytes();
 int walk_slots_per_sm(const WsLayout& ws);
 int launch_flow_jobs(const DevFlowJob* d_jobs, int32_t count, char* d_ws, const WsLayout& ws,
                      int32_t slots, void* stream);

@@ -99,6 +99,8 @@ __device__ __forceinline__ void red_add(long long* p, long long d) {
 }
 
 __device__ __forceinline__ long long now() { return clock64(); }
+// L1 prefetch of the line holding p (global); no value returned, never faults.
+__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -133,6 +135,7 @@ struct Net {
   int2* lg;        // BFS log: {position used to reach the node, parent log index}
   int4* fglob;     // frontier overflow, 2 buffers of fstride entries
   uint32_t s_bits;  // smem (shared-window address) visited bitset
+  uint32_t s_pok;   // smem bitset: node x < 2n whose computation arc to x ^ 1 has residual > 0
   uint32_t s_fs;    // smem frontier, 2 buffers of kFrontCap int4 entries
   int2* ends;       // smem: phase-B arcs into the sink {position, parent log index}
   int32_t* path;
@@ -160,6 +163,11 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ void atoms_and(uint32_t a, uint32_t m) {
+  asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a), "r"(m) : "memory");
+}
+// Static incidence entry through the read-only path as one 16 B load.
+__device__ __forceinline__ int4 ldg_ient(const IEnt* p) { return __ldg(reinterpret_cast<const int4*>(p)); }
 __device__ __forceinline__ uint32_t atoms_or(uint32_t a, uint32_t m) {
   uint32_t old;
   asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(m) : "memory");
@@ -186,6 +194,8 @@ __device__ __forceinline__ bool test_and_set(Net& N, int u) {
   const uint32_t m = 1u << (u & 31);
   return (atoms_or(N.s_bits + 4u * (u >> 5), m) & m) == 0;
 }
+__device__ __forceinline__ void pok_set(Net& N, int x) { atoms_or(N.s_pok + 4u * (x >> 5), 1u << (x & 31)); }
+__device__ __forceinline__ void pok_clear(Net& N, int x) { atoms_and(N.s_pok + 4u * (x >> 5), ~(1u << (x & 31))); }
 __device__ __forceinline__ bool bit_of(const Net& N, int u) {
   return (lds32(N.s_bits + 4u * (u >> 5)) >> (u & 31)) & 1u;
 }
@@ -210,7 +220,7 @@ __device__ int collect_ends(Net& N, int buf, int cnt) {
     for (int r = 0; r < rounds; ++r) {
       const int p = fe.y + r;
       bool end = false;
-      if (p < fe.z && N.ient[p].other == N.snk) {
+      if (p < fe.z && ldg_ient(N.ient + p).x == N.snk) {
         const long long w = N.resid[p];
         end = w != 0 && w >= negS;
       }
@@ -264,39 +274,76 @@ __device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
       arcs += mine;
       for (int r = 0; r < rounds; ++r, p += g) {
         const bool v = p < fe.z;
-        IEnt e{0, 0, 0, 0};
+        int4 e = make_int4(0, 0, 0, 0);  // {other, packed twin, other_off, other_end}
         long long w = 0;
         if (v) {
-          e = N.ient[p];
+          e = ldg_ient(N.ient + p);
           w = N.resid[p];
         }
         const bool ok = w != 0 && w >= negS;
-        const uint32_t m = ok ? 1u << (e.other & 31) : 0u;
-        const uint32_t o = atoms_or(N.s_bits + 4u * (e.other >> 5), m);
+        const uint32_t m = ok ? 1u << (e.x & 31) : 0u;
+        const uint32_t o = atoms_or(N.s_bits + 4u * (e.x >> 5), m);
         const bool c = ok && (o & m) == 0;
+        // partner shortcut: a new node y = e.x whose computation arc (first in
+        // its list, position e.z) has residual also reaches z = y ^ 1 in this
+        // level; z's list is adjacent to y's (pd = its degree)
+        const int pd = static_cast<int>(static_cast<unsigned>(e.y) >> kPdegShift);
+        bool cz = false;
+        if (c && pd != kNoPartner && ((lds32(N.s_pok + 4u * (e.x >> 5)) >> (e.x & 31)) & 1u))
+          cz = test_and_set(N, e.x ^ 1);
         const unsigned bm = __ballot_sync(kFull, c);
+        const unsigned bz = __ballot_sync(kFull, cz);
         const int pos = nc + __popc(bm & lt);
-        bool hit = false;
+        const int posz = nc + __popc(bm) + __popc(bz & lt);
+        int hitli = -1, hitnode = -1;
         if (c) {
           const int li = nlog + pos;
           N.lg[li] = make_int2(p, fe.w);
-          const int4 ent = make_int4(e.other, e.other_off, e.other_end, li);
+          const int4 ent = make_int4(e.x, e.z, e.w, li);
+          // the next level reads this node's arcs: start their DRAM->L1 fill now
+          pf_l1(N.ient + e.z);
+          pf_l1(N.ient + e.w - 1);
+          pf_l1(N.resid + e.z);
+          pf_l1(N.resid + e.w - 1);
           if (pos < kFrontCap)
             sts128(fnxt + 16u * pos, ent);
           else
             gnxt[pos] = ent;
-          if (kA) hit = N.bal[e.other] < 0;
-        }
-        if (kA) {
-          const unsigned h = __ballot_sync(kFull, hit);
-          if (h && found < 0) {
-            const int hl = __ffs(h) - 1;
-            found = __shfl_sync(kFull, nlog + pos, hl);
-            tgt = __shfl_sync(kFull, e.other, hl);
+          if (kA && N.bal[e.x] < 0) {
+            hitli = li;
+            hitnode = e.x;
           }
         }
-        nc += __popc(bm);
-        upd += c;
+        if (cz) {
+          const int z = e.x ^ 1;
+          const int zo = (e.x & 1) ? e.z - pd : e.w;
+          const int ze = (e.x & 1) ? e.z : e.w + pd;
+          const int lz = nlog + posz;
+          N.lg[lz] = make_int2(e.z, nlog + pos);  // via y's computation arc
+          const int4 ent = make_int4(z, zo, ze, lz);
+          pf_l1(N.ient + zo);
+          pf_l1(N.ient + ze - 1);
+          pf_l1(N.resid + zo);
+          pf_l1(N.resid + ze - 1);
+          if (posz < kFrontCap)
+            sts128(fnxt + 16u * posz, ent);
+          else
+            gnxt[posz] = ent;
+          if (kA && hitli < 0 && N.bal[z] < 0) {
+            hitli = lz;
+            hitnode = z;
+          }
+        }
+        if (kA) {
+          const unsigned h = __ballot_sync(kFull, hitli >= 0);
+          if (h && found < 0) {
+            const int hl = __ffs(h) - 1;
+            found = __shfl_sync(kFull, hitli, hl);
+            tgt = __shfl_sync(kFull, hitnode, hl);
+          }
+        }
+        nc += __popc(bm) + __popc(bz);
+        upd += c + cz;
       }
     }
     __syncwarp();
@@ -355,8 +402,15 @@ __device__ long long push_chain(Net& N, int first, int idx, long long cap, bool 
   if (d <= 0) return 0;
   for (int q = ln; q < k; q += 32) {
     const int p = N.path[q];
-    N.resid[p] -= d;
-    N.resid[N.ient[p].twin] += d;
+    const int4 e = ldg_ient(N.ient + p);
+    const long long nv = N.resid[p] - d;
+    N.resid[p] = nv;
+    N.resid[e.y & kTwinMask] += d;
+    if (e.y & kCompArc) {
+      // computation arc owner -> e.x (owner = e.x ^ 1): keep the shortcut bits exact
+      if (eff_res(nv, N.S) <= 0) pok_clear(N, e.x ^ 1);
+      pok_set(N, e.x);
+    }
   }
   __syncwarp();
   C.add(kPrPaths, 1);
@@ -877,6 +931,19 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
     }
   }
   __syncwarp();
+  // shortcut bits of the rebuilt computation arcs (exact now that S is known);
+  // when a carried flow may reach the sentinel, rebuild them all
+  const bool all = N.R >= N.S;
+  const int cnt = all ? n : nh;
+  for (int k = ln; k < cnt; k += 32) {
+    const int i = all ? k : W.delta[k];
+    const CompRec rc = I.crec[i];
+    const bool fwd = W.ecrit[i] && eff_res(N.resid[rc.pt], N.S) > 0;
+    const bool bwd = W.ecrit[i] && N.resid[rc.ph] > 0;
+    if (fwd) pok_set(N, 2 * i); else pok_clear(N, 2 * i);
+    if (bwd) pok_set(N, 2 * i + 1); else pok_clear(N, 2 * i + 1);
+  }
+  __syncwarp();
   C.add(kPrCap, now() - t0);
   return PB_OK;
 }
@@ -899,6 +966,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   for (int v = ln; v < I.V; v += 32) N.bal[v] = 0;
   for (int e = ln; e < I.E; e += 32) W.ecrit[e] = 0;
   for (int i = ln; i < n; i += 32) W.dirty[i] = 0;
+  for (int w = ln; w < N.nbitw; w += 32) sts32(N.s_pok + 4u * w, 0u);
 
   int bad = 0;
   long long spe = 0, spt = 0, sre = 0, srt = 0;
@@ -1137,6 +1205,7 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   p.N.s_fs = sa + 8 * kMaxEnds;
   p.N.s_bits = sa + 8 * kMaxEnds + 16 * 2 * kFrontCap;
+  p.N.s_pok = p.N.s_bits + static_cast<uint32_t>((4 * ((L.max_v + 31) / 32) + 15) / 16 * 16);
   return p;
 }
 
@@ -1172,19 +1241,40 @@ __device__ __forceinline__ char* my_smem(const WsLayout& L, unsigned long long**
 __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel(const DevInst* insts, int n_inst,
                                                       const int32_t* order, int32_t* counter,
                                                       char* ws_base, WsLayout L, int slots,
-                                                      RunCounters* ctr, DeltaPool pool) {
+                                                      RunCounters* ctr, DeltaPool pool, int n_big) {
   const int slot = warp_slot();
   if (slot >= slots) return;
+  if (n_big > 0 && lane_id() == 0) {
+    // let the exclusive-SM CTAs land first (bounded: never waits > 200 us)
+    const unsigned long long t0 = gtimer();
+    while (*reinterpret_cast<volatile int32_t*>(counter + 1) < n_big && gtimer() - t0 < 200000ull) __nanosleep(1000);
+  }
+  __syncwarp();
   Counters C;
   char* sm = my_smem(L, &C.prof);
-  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(slot) * L.stride, L, sm);
+  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(n_big + slot) * L.stride, L, sm);
   for (;;) {
     int k = 0;
-    if (lane_id() == 0) k = atomicAdd(counter, 1);
+    if (lane_id() == 0) k = n_big + atomicAdd(counter, 1);
     k = __shfl_sync(kFull, k, 0);
     if (k >= n_inst) break;
     run_walk(insts[order[k]], P.N, P.W, pool, C);
   }
+  flush_counters(C, ctr);
+}
+
+// Exclusive-SM walks: one warp per CTA, blockIdx.x-th instance of the
+// order; the CTA requests (nearly) all of the SM's shared memory so that no
+// walker CTA is co-resident.  Started first; walkers wait (bounded) until
+// the big CTAs are resident so that they cannot take those SMs.
+__global__ void __launch_bounds__(32) walk_kernel_big(const DevInst* insts, const int32_t* order,
+                                                      char* ws_base, WsLayout L, RunCounters* ctr,
+                                                      DeltaPool pool, int32_t* resident) {
+  Counters C;
+  char* sm = my_smem(L, &C.prof);
+  if (lane_id() == 0) atomicAdd(resident, 1);
+  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(blockIdx.x) * L.stride, L, sm);
+  run_walk(insts[order[blockIdx.x]], P.N, P.W, pool, C);
   flush_counters(C, ctr);
 }
 
@@ -1392,13 +1482,29 @@ int walk_slots_per_sm(const WsLayout& ws) {
   return blocks * kWarpsPerBlock;
 }
 
+int big_walk_smem_bytes() {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return optin;
+}
+
+// d_counter[0] = walker queue cursor, d_counter[1] = resident big CTAs.
 int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
                  char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
-                 DeltaPool pool, void* stream) {
-  const size_t sm = block_smem(ws);
-  set_smem(walk_kernel, sm);
-  walk_kernel<<<blocks_for(slots), kBlock, sm, static_cast<cudaStream_t>(stream)>>>(
-      d_insts, n_inst, d_order, d_counter, d_ws, ws, slots, d_counters, pool);
+                 DeltaPool pool, int32_t n_big, void* stream, void* stream_big) {
+  if (n_big > 0) {
+    const int sm_big = big_walk_smem_bytes();
+    set_smem(walk_kernel_big, sm_big);
+    walk_kernel_big<<<n_big, 32, sm_big, static_cast<cudaStream_t>(stream_big)>>>(
+        d_insts, d_order, d_ws, ws, d_counters, pool, d_counter + 1);
+  }
+  if (n_inst > n_big) {
+    const size_t sm = block_smem(ws);
+    set_smem(walk_kernel, sm);
+    walk_kernel<<<blocks_for(slots), kBlock, sm, static_cast<cudaStream_t>(stream)>>>(
+        d_insts, n_inst, d_order, d_counter, d_ws, ws, slots, d_counters, pool, n_big);
+  }
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -23,6 +23,13 @@ def profile(name):
         k, _, reps = name[len("config"):].partition("*")
         for _ in range(int(reps or 1)):
             b.add_g9(g9.named_config(int(k)))
+    elif name.startswith("rep:"):  # rep:3284:148 = 148 copies of config-5 instance 3284
+        _, i, r = name.split(":")
+        for _ in range(int(r)):
+            b.add_g9(g9.batch_params(int(i)))
+    elif name.startswith("inst:"):  # single config-5 instances: inst:3284[,1580...]
+        for i in name.split(":")[1].split(","):
+            b.add_g9(g9.batch_params(int(i)))
     elif name.startswith("batch:"):
         for i in range(int(name.split(":")[1])):
             b.add_g9(g9.batch_params(i))
