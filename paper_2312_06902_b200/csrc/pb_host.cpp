@@ -296,6 +296,11 @@ uint64_t bits(double d) {
   return u;
 }
 
+// Cooperative (wide) walk plan, see choose_wide().
+struct WidePlan {
+  int32_t n = 0, ctas = 0, warps = 4;
+};
+
 struct DeviceRun {
   int device = -1;
   char* d_static = nullptr;
@@ -314,7 +319,7 @@ struct DeviceRun {
   pb::WsLayout ws{};
   cudaStream_t stream = nullptr, stream_big = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_big = nullptr;
-  int32_t n_big = 0;
+  WidePlan wide;
   char* h_out = nullptr;  // pinned
   void release() {
     if (device < 0) return;
@@ -561,29 +566,38 @@ int env_int(const char* name, int dflt) {
   return e && *e ? std::atoi(e) : dflt;
 }
 
-// Exclusive-SM walks (pb_internal.h launch_walks): the LPT head whose
-// estimated work is within PB_BIG_FRAC (default 0.9) of the largest, at most
-// a quarter of the SMs, and only for batches that fill the device.
-// PB_BIG overrides the count.
-int32_t choose_big(const pb_batch* b, const std::vector<int32_t>& order, int sms, int per_sm) {
+// Cooperative (wide) walks, pb_internal.h launch_walks: the LPT head.
+// PB_WIDE = number of instances (default: those whose estimated work is at
+// least PB_WIDE_PERMILLE of the largest, only for batches that fill the
+// device), PB_WIDE_CTAS = concurrent wide walks, PB_WIDE_WARPS = warps each.
+WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int sms, int per_sm) {
+  WidePlan w;
   const int64_t N = static_cast<int64_t>(order.size());
-  int big = env_int("PB_BIG", 0);  // measured: no gain, off by default
-  if (big < 0) {
-    big = 0;
-    if (N > int64_t{sms} * per_sm / 2 && N > 0) {
-      const double frac = env_int("PB_BIG_PERMILLE", 900) / 1000.0;
+  w.warps = std::max(2, std::min(4, env_int("PB_WIDE_WARPS", 4)));
+  int n = env_int("PB_WIDE", -1);
+  if (n < 0) {
+    n = 0;
+    const int permille = env_int("PB_WIDE_PERMILLE", 0);
+    if (permille > 0 && N > int64_t{sms} * per_sm) {
       const double top = static_cast<double>(b->insts[order[0]].work);
-      while (big < sms / 4 && big < N && static_cast<double>(b->insts[order[big]].work) >= frac * top) ++big;
+      while (n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;
     }
   }
-  return static_cast<int32_t>(std::min<int64_t>({int64_t{big}, N, int64_t{sms}}));
+  w.n = static_cast<int32_t>(std::min<int64_t>(n, N));
+  const int ctas = env_int("PB_WIDE_CTAS", sms);
+  w.ctas = w.n > 0 ? std::max(1, std::min(ctas, w.n)) : 0;
+  return w;
 }
 
-int32_t device_slots(int device, int64_t n_walk, const pb::WsLayout& ws, int32_t n_big) {
+// Walker warps: what is left of the device after the wide CTAs (4-warp
+// blocks, like the walker's).
+int32_t device_slots(int device, int64_t n_walk, const pb::WsLayout& ws, const WidePlan& w) {
   int sms = 0;
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   const int per_sm = std::max(1, env_int("PB_WARPS_PER_SM", pb::walk_slots_per_sm(ws)));
-  return static_cast<int32_t>(std::min<int64_t>(n_walk, int64_t{sms - n_big} * per_sm));
+  const int64_t wide_warps = int64_t{w.ctas} * w.warps;
+  return static_cast<int32_t>(
+      std::max<int64_t>(std::min<int64_t>(n_walk, int64_t{sms} * per_sm - wide_warps), std::min<int64_t>(n_walk, 4)));
 }
 
 pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
@@ -615,10 +629,10 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   {
     int sms = 0;
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
-    R.n_big = choose_big(b, P.order, sms, std::max(1, pb::walk_slots_per_sm(R.ws)));
+    R.wide = choose_wide(b, P.order, sms, std::max(1, pb::walk_slots_per_sm(R.ws)));
   }
-  R.slots = device_slots(device, static_cast<int64_t>(N) - R.n_big, R.ws, R.n_big);
-  ck(cudaMalloc(&R.d_ws, static_cast<size_t>(R.ws.stride) * (R.slots + R.n_big)), "malloc workspace");
+  R.slots = device_slots(device, static_cast<int64_t>(N) - R.wide.n, R.ws, R.wide);
+  ck(cudaMalloc(&R.d_ws, static_cast<size_t>(R.ws.stride) * (R.slots + R.wide.ctas)), "malloc workspace");
   ck(cudaMalloc(&R.d_insts, sizeof(pb::DevInst) * N), "malloc insts");
   ck(cudaMalloc(&R.d_order, sizeof(int32_t) * N), "malloc order");
   ck(cudaMalloc(&R.d_counter, 2 * sizeof(int32_t)), "malloc counter");
@@ -666,8 +680,8 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   ck(cudaEventRecord(R.ev0, R.stream), "record");
   ck(cudaStreamWaitEvent(R.stream_big, R.ev0, 0), "wait");
   const int rc = pb::launch_walks(R.d_insts, static_cast<int32_t>(N), R.d_order, R.d_counter,
-                                  R.d_ws, R.ws, R.slots, R.d_counters, pool, R.n_big, R.stream,
-                                  R.stream_big);
+                                  R.d_ws, R.ws, R.slots, R.d_counters, pool, R.wide.n, R.wide.ctas,
+                                  R.wide.warps, R.stream, R.stream_big);
   if (rc != 0) throw CudaError(std::string("walk launch: ") + cudaGetErrorString(static_cast<cudaError_t>(rc)));
   ck(cudaEventRecord(R.ev_big, R.stream_big), "record");
   ck(cudaStreamWaitEvent(R.stream, R.ev_big, 0), "wait");
@@ -683,7 +697,7 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   b->stats.rounds = static_cast<int64_t>(rcnt.rounds);
   b->stats.comp_visits = static_cast<int64_t>(rcnt.comp_visits);
   for (int q = 0; q < pb::kPrSlots; ++q) b->prof[q] = static_cast<int64_t>(rcnt.prof[q]);
-  b->stats.kernel_launches += (R.n_big > 0 ? 1 : 0) + (static_cast<int32_t>(N) > R.n_big ? 1 : 0);
+  b->stats.kernel_launches += (R.wide.n > 0 ? 1 : 0) + (static_cast<int32_t>(N) > R.wide.n ? 1 : 0);
   if (kernel_ms) *kernel_ms = ms;
   return PB_OK;
 }

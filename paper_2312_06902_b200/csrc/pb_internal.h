@@ -143,7 +143,7 @@ struct WsLayout {
   int64_t max_n, max_v, max_e;
   int64_t off_resid;                   // int64 [2E] residual by position
   int64_t off_bal;                     // int64 [V] phase-A imbalance
-  int64_t off_log;                     // int2  [V] BFS log {position, parent log index}
+  int64_t off_log;                     // int4  [V] BFS log {arc, arc before or -1, parent, 0}
   int64_t off_front;                   // int4  [2V] frontier overflow (ping-pong)
   int64_t off_ecrit;                   // u8    [E] edge critical in the current network
   int64_t off_durp, off_durr;          // int64 [n]
@@ -179,7 +179,7 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   };
   L.off_resid = take(8 * 2 * max_e);
   L.off_bal = take(8 * max_v);
-  L.off_log = take(8 * max_v);
+  L.off_log = take(16 * max_v);
   L.off_front = take(16 * 2 * max_v);
   L.off_ecrit = take(max_e);
   L.off_durp = take(8 * max_n);
@@ -233,15 +233,15 @@ struct SlackOut {
 
 // Host-side launchers (pb_kernels.cu).  slots = number of walker warps (one
 // workspace each).
-// The first n_big instances of the LPT order run in a separate launch of
-// one-warp CTAs that claim a whole SM's shared memory each (exclusive SMs:
-// the longest walks bound the batch and must not share an SM); the rest run
-// in the persistent walker kernel (`slots` warps) on the remaining SMs.
-// Workspace slots: [0, n_big) big walks, [n_big, n_big + slots) walkers.
+// The first n_wide instances of the LPT order (the longest walks, which
+// bound the batch) run in walk_kernel_wide: wide_ctas CTAs of wide_warps
+// warps, one walk per CTA, every BFS expanded by all its warps; the rest run
+// in the persistent walker kernel (`slots` warps, one walk each).
+// Workspace slots: [0, wide_ctas) wide CTAs, [wide_ctas, +slots) walkers.
 int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
                  char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
-                 DeltaPool pool, int32_t n_big, void* stream, void* stream_big);
-int big_walk_smem_bytes();
+                 DeltaPool pool, int32_t n_wide, int32_t wide_ctas, int32_t wide_warps, void* stream,
+                 void* stream_wide);
 int walk_slots_per_sm(const WsLayout& ws);
 int launch_flow_jobs(const DevFlowJob* d_jobs, int32_t count, char* d_ws, const WsLayout& ws,
                      int32_t slots, void* stream);

@@ -132,7 +132,7 @@ struct Net {
   const IEnt* ient;
   long long* resid;
   long long* bal;
-  int2* lg;        // BFS log: {position used to reach the node, parent log index}
+  int4* lg;        // BFS log: {arc into the node, arc before it or -1, parent log index, 0}
   int4* fglob;     // frontier overflow, 2 buffers of fstride entries
   uint32_t s_bits;  // smem (shared-window address) visited bitset
   uint32_t s_pok;   // smem bitset: node x < 2n whose computation arc to x ^ 1 has residual > 0
@@ -143,7 +143,24 @@ struct Net {
   int32_t* exl;
   long long S;  // infinity sentinel of the current network
   long long R;  // flow on the return arc = s->t value
+  struct CoopCtl* ctl;  // cooperative BFS (nw > 1 warps of one CTA), else null
+  int nw;
 };
+
+// Control block of a cooperative walk CTA (shared memory): warp 0 drives the
+// walk and posts each BFS as a job; helper warps join it.
+struct CoopCtl {
+  int cmd;   // 0 exit, 1 BFS phase B, 2 BFS phase A
+  int nsrc;
+  long long S;
+  const DevInst* inst;
+  int nc[3];                 // next-level sizes, rotating by level
+  unsigned long long found;  // phase A: (log index << 32) | node, ~0 = none
+};
+
+__device__ __forceinline__ void bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // Explicit shared-memory accessors (the smem base travels in a struct, so
 // plain pointers would compile to generic LD/ST).
@@ -203,7 +220,7 @@ __device__ __forceinline__ bool bit_of(const Net& N, int u) {
 // Seeds frontier slot k (buffer 0) and log entry k with node v.
 __device__ __forceinline__ void seed(Net& N, int k, int v) {
   fwrite(N, 0, k, make_int4(v, N.inc_off[v], N.inc_off[v + 1], k));
-  N.lg[k] = make_int2(-1 - v, -1);
+  N.lg[k] = make_int4(-1 - v, -1, -1, 0);
 }
 
 // Phase B: the arcs of frontier buffer buf (cnt entries) that enter the sink
@@ -244,10 +261,23 @@ __device__ int collect_ends(Net& N, int buf, int cnt) {
 // the level that marks the sink (one shared load per level) and returns the
 // number of that level's arcs into the sink, recorded in N.ends (0 = sink
 // unreachable; the bitset then marks exactly the residual-reachable set).
-template <bool kA>
-__device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
+// Level-synchronous BFS over residual arcs from the nsrc seeded sources
+// (already marked).  g = 1, 2 or 4 lanes share a frontier node and take its
+// arcs round-robin; per arc one {ient, resid} load pair, one unconditional
+// shared atomic test-and-set (mask 0 for non-arcs), the partner shortcut and
+// one ballot.  The frontier lives in shared memory (spilling to global past
+// kFrontCap).  kCoop: the nw warps of the CTA split every level (next-level
+// slots from a shared counter, one named barrier per level); warp wi.
+// Phase A (kA): targets are nodes with bal < 0; stops after the level that
+// reaches one and returns its log index (tgt = node).  Phase B: stops after
+// the level that marks the sink (one shared load per level) and returns the
+// number of that level's arcs into the sink, recorded in N.ends (0 = sink
+// unreachable; the bitset then marks exactly the residual-reachable set).
+template <bool kA, bool kCoop>
+__device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi) {
   const int ln = lane_id();
   const unsigned lt = lanemask_lt();
+  const int nw = kCoop ? N.nw : 1;
   const long long t0 = now();
   const long long negS = -N.S;  // raw residual r is positive iff r != 0 && r >= -S
   int cnt = nsrc, cur = 0, nlog = nsrc, found = -1, levels = 0, prev = 0;
@@ -255,16 +285,19 @@ __device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
   tgt = -1;
   const uint32_t snk_word = N.s_bits + 4u * (N.snk >> 5), snk_mask = 1u << (N.snk & 31);
   while (cnt > 0) {
-    ++levels;
-    const int lg2 = cnt <= 8 ? 2 : (cnt <= 16 ? 1 : 0);
+    const int per = kCoop ? (cnt + nw - 1) / nw : cnt;
+    const int lg2 = per <= 8 ? 2 : (per <= 16 ? 1 : 0);
     const int g = 1 << lg2;
     const int sub = ln & (g - 1);
     const int nxt = cur ^ 1;
     const uint32_t fcur = N.s_fs + 16u * kFrontCap * cur, fnxt = N.s_fs + 16u * kFrontCap * nxt;
     int4* gcur = N.fglob + static_cast<size_t>(cur) * N.fstride;
     int4* gnxt = N.fglob + static_cast<size_t>(nxt) * N.fstride;
+    int* ncp = kCoop ? &N.ctl->nc[levels % 3] : nullptr;
+    if (kCoop && wi == 0 && ln == 0) N.ctl->nc[(levels + 1) % 3] = 0;
+    ++levels;
     int nc = 0;
-    for (int base = 0; base < cnt; base += 32 >> lg2) {
+    for (int base = wi * (32 >> lg2); base < cnt; base += nw * (32 >> lg2)) {
       const int slot = base + (ln >> lg2);
       int4 fe = make_int4(0, 0, 0, 0);
       if (slot < cnt) fe = slot < kFrontCap ? lds128(fcur + 16u * slot) : gcur[slot];
@@ -282,6 +315,7 @@ __device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
         }
         const bool ok = w != 0 && w >= negS;
         const uint32_t m = ok ? 1u << (e.x & 31) : 0u;
+        const uint32_t pw = lds32(N.s_pok + 4u * (e.x >> 5));  // issued beside the atomic
         const uint32_t o = atoms_or(N.s_bits + 4u * (e.x >> 5), m);
         const bool c = ok && (o & m) == 0;
         // partner shortcut: a new node y = e.x whose computation arc (first in
@@ -289,22 +323,25 @@ __device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
         // level; z's list is adjacent to y's (pd = its degree)
         const int pd = static_cast<int>(static_cast<unsigned>(e.y) >> kPdegShift);
         bool cz = false;
-        if (c && pd != kNoPartner && ((lds32(N.s_pok + 4u * (e.x >> 5)) >> (e.x & 31)) & 1u))
-          cz = test_and_set(N, e.x ^ 1);
+        if (c && pd != kNoPartner && ((pw >> (e.x & 31)) & 1u)) cz = test_and_set(N, e.x ^ 1);
         const unsigned bm = __ballot_sync(kFull, c);
         const unsigned bz = __ballot_sync(kFull, cz);
-        const int pos = nc + __popc(bm & lt);
-        const int posz = nc + __popc(bm) + __popc(bz & lt);
+        int b0 = nc;
+        if (kCoop) {
+          const int t = __popc(bm) + __popc(bz);
+          if (ln == 0 && t) b0 = atomicAdd(ncp, t);
+          b0 = __shfl_sync(kFull, b0, 0);
+        }
+        const int pos = b0 + __popc(bm & lt);
+        const int posz = b0 + __popc(bm) + __popc(bz & lt);
         int hitli = -1, hitnode = -1;
         if (c) {
           const int li = nlog + pos;
-          N.lg[li] = make_int2(p, fe.w);
+          N.lg[li] = make_int4(p, -1, fe.w, 0);
           const int4 ent = make_int4(e.x, e.z, e.w, li);
           // the next level reads this node's arcs: start their DRAM->L1 fill now
           pf_l1(N.ient + e.z);
-          pf_l1(N.ient + e.w - 1);
           pf_l1(N.resid + e.z);
-          pf_l1(N.resid + e.w - 1);
           if (pos < kFrontCap)
             sts128(fnxt + 16u * pos, ent);
           else
@@ -319,12 +356,10 @@ __device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
           const int zo = (e.x & 1) ? e.z - pd : e.w;
           const int ze = (e.x & 1) ? e.z : e.w + pd;
           const int lz = nlog + posz;
-          N.lg[lz] = make_int2(e.z, nlog + pos);  // via y's computation arc
+          N.lg[lz] = make_int4(e.z, p, fe.w, 0);  // y's computation arc, the arc into y, y's parent
           const int4 ent = make_int4(z, zo, ze, lz);
           pf_l1(N.ient + zo);
-          pf_l1(N.ient + ze - 1);
           pf_l1(N.resid + zo);
-          pf_l1(N.resid + ze - 1);
           if (posz < kFrontCap)
             sts128(fnxt + 16u * posz, ent);
           else
@@ -336,30 +371,74 @@ __device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
         }
         if (kA) {
           const unsigned h = __ballot_sync(kFull, hitli >= 0);
-          if (h && found < 0) {
+          if (h) {
             const int hl = __ffs(h) - 1;
-            found = __shfl_sync(kFull, hitli, hl);
-            tgt = __shfl_sync(kFull, hitnode, hl);
+            const int fl = __shfl_sync(kFull, hitli, hl);
+            const int fn = __shfl_sync(kFull, hitnode, hl);
+            if (kCoop) {
+              if (ln == 0)
+                atomicMin(&N.ctl->found, (static_cast<unsigned long long>(fl) << 32) | static_cast<unsigned>(fn));
+            } else if (found < 0) {
+              found = fl;
+              tgt = fn;
+            }
           }
         }
-        nc += __popc(bm) + __popc(bz);
+        if (!kCoop) nc += __popc(bm) + __popc(bz);
         upd += c + cz;
       }
     }
-    __syncwarp();
+    if (kCoop) {
+      bar_sync(1, 32 * nw);
+      nc = *reinterpret_cast<volatile int*>(ncp);
+    } else {
+      __syncwarp();
+    }
     nlog += nc;
     prev = cnt;
     cnt = nc;
     cur = nxt;
-    if (kA ? found >= 0 : (lds32(snk_word) & snk_mask) != 0) break;
+    bool done;
+    if (kA) {
+      if (kCoop) {
+        const unsigned long long f = *reinterpret_cast<volatile unsigned long long*>(&N.ctl->found);
+        if (f != ~0ull) {
+          found = static_cast<int>(f >> 32);
+          tgt = static_cast<int>(f & 0xffffffffu);
+        }
+      }
+      done = found >= 0;
+    } else {
+      done = (lds32(snk_word) & snk_mask) != 0;
+    }
+    if (done) break;
   }
+  if (kCoop) bar_sync(2, 32 * nw);  // every warp is past its last read of shared state
   C.arc_scans += arcs;
   C.node_updates += upd;
   C.add(kPrBfsLevels, levels);
   int ret = found;
-  if (!kA) ret = (lds32(snk_word) & snk_mask) ? collect_ends(N, cur ^ 1, prev) : 0;
+  if (!kA) ret = (wi == 0 && (lds32(snk_word) & snk_mask)) ? collect_ends(N, cur ^ 1, prev) : 0;
   C.add(kPrBfs, now() - t0);
   return ret;
+}
+
+// BFS entry for the walk driver (warp 0): solo, or posted to the CTA's
+// helper warps (walk_kernel_wide) and run cooperatively.
+template <bool kA>
+__device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
+  if (N.nw <= 1) return bfs_core<kA, false>(N, nsrc, tgt, C, 0);
+  if (lane_id() == 0) {
+    CoopCtl* k = N.ctl;
+    k->cmd = kA ? 2 : 1;
+    k->nsrc = nsrc;
+    k->S = N.S;
+    k->nc[0] = 0;
+    k->found = ~0ull;
+  }
+  __syncwarp();
+  bar_sync(1, 32 * N.nw);  // release the helpers
+  return bfs_core<kA, true>(N, nsrc, tgt, C, 0);
 }
 
 // Pushes flow along a chain: position `first` (if >= 0), then the logged
@@ -375,13 +454,14 @@ __device__ long long push_chain(Net& N, int first, int idx, long long cap, bool 
   if (ln == 0) {
     if (first >= 0) N.path[k++] = first;
     for (;;) {
-      const int2 l = N.lg[idx];
+      const int4 l = N.lg[idx];
       if (l.x < 0) {
         s = -1 - l.x;
         break;
       }
       N.path[k++] = l.x;
-      idx = l.y;
+      if (l.y >= 0) N.path[k++] = l.y;  // shortcut entry: two arcs per hop
+      idx = l.z;
     }
   }
   k = __shfl_sync(kFull, k, 0);
@@ -1185,7 +1265,7 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   WsPtrs p;
   p.N.resid = reinterpret_cast<long long*>(base + L.off_resid);
   p.N.bal = reinterpret_cast<long long*>(base + L.off_bal);
-  p.N.lg = reinterpret_cast<int2*>(base + L.off_log);
+  p.N.lg = reinterpret_cast<int4*>(base + L.off_log);
   p.N.fglob = reinterpret_cast<int4*>(base + L.off_front);
   p.N.fstride = static_cast<int>(L.max_v);
   p.N.path = reinterpret_cast<int32_t*>(base + L.off_path);
@@ -1206,6 +1286,8 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.N.s_fs = sa + 8 * kMaxEnds;
   p.N.s_bits = sa + 8 * kMaxEnds + 16 * 2 * kFrontCap;
   p.N.s_pok = p.N.s_bits + static_cast<uint32_t>((4 * ((L.max_v + 31) / 32) + 15) / 16 * 16);
+  p.N.ctl = nullptr;
+  p.N.nw = 1;
   return p;
 }
 
@@ -1241,21 +1323,16 @@ __device__ __forceinline__ char* my_smem(const WsLayout& L, unsigned long long**
 __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel(const DevInst* insts, int n_inst,
                                                       const int32_t* order, int32_t* counter,
                                                       char* ws_base, WsLayout L, int slots,
-                                                      RunCounters* ctr, DeltaPool pool, int n_big) {
+                                                      RunCounters* ctr, DeltaPool pool, int n_wide,
+                                                      int ws_first) {
   const int slot = warp_slot();
   if (slot >= slots) return;
-  if (n_big > 0 && lane_id() == 0) {
-    // let the exclusive-SM CTAs land first (bounded: never waits > 200 us)
-    const unsigned long long t0 = gtimer();
-    while (*reinterpret_cast<volatile int32_t*>(counter + 1) < n_big && gtimer() - t0 < 200000ull) __nanosleep(1000);
-  }
-  __syncwarp();
   Counters C;
   char* sm = my_smem(L, &C.prof);
-  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(n_big + slot) * L.stride, L, sm);
+  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(ws_first + slot) * L.stride, L, sm);
   for (;;) {
     int k = 0;
-    if (lane_id() == 0) k = n_big + atomicAdd(counter, 1);
+    if (lane_id() == 0) k = n_wide + atomicAdd(counter, 1);
     k = __shfl_sync(kFull, k, 0);
     if (k >= n_inst) break;
     run_walk(insts[order[k]], P.N, P.W, pool, C);
@@ -1263,18 +1340,55 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel(const DevInst*
   flush_counters(C, ctr);
 }
 
-// Exclusive-SM walks: one warp per CTA, blockIdx.x-th instance of the
-// order; the CTA requests (nearly) all of the SM's shared memory so that no
-// walker CTA is co-resident.  Started first; walkers wait (bounded) until
-// the big CTAs are resident so that they cannot take those SMs.
-__global__ void __launch_bounds__(32) walk_kernel_big(const DevInst* insts, const int32_t* order,
-                                                      char* ws_base, WsLayout L, RunCounters* ctr,
-                                                      DeltaPool pool, int32_t* resident) {
+// Cooperative walks for the longest instances (their walk time bounds the
+// batch): a CTA of nw warps per walk.  Warp 0 drives run_walk; every BFS is
+// posted to the CTA's control block and expanded by all nw warps
+// (bfs_core<., true>); the other phases stay on warp 0.  The walk's shared
+// structures (frontier, bitsets, path ends) are warp 0's region.
+__global__ void __launch_bounds__(kBlock) walk_kernel_wide(const DevInst* insts, int n_wide,
+                                                           const int32_t* order, int32_t* counter,
+                                                           char* ws_base, WsLayout L, RunCounters* ctr,
+                                                           DeltaPool pool) {
+  const int nw = blockDim.x >> 5;
+  const int wi = warp_in_block();
   Counters C;
-  char* sm = my_smem(L, &C.prof);
-  if (lane_id() == 0) atomicAdd(resident, 1);
-  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(blockIdx.x) * L.stride, L, sm);
-  run_walk(insts[order[blockIdx.x]], P.N, P.W, pool, C);
+  (void)my_smem(L, &C.prof);  // this warp's profile slots
+  const int per = 128 + 8 * kMaxEnds + L.smem_bytes;
+  CoopCtl* ctl = reinterpret_cast<CoopCtl*>(g_smem + nw * per);
+  WsPtrs P = bind_ws(ws_base + static_cast<size_t>(blockIdx.x) * L.stride, L, g_smem + 128);
+  P.N.ctl = ctl;
+  P.N.nw = nw;
+  if (wi == 0) {
+    for (;;) {
+      int k = 0;
+      if (lane_id() == 0) k = atomicAdd(counter + 1, 1);
+      k = __shfl_sync(kFull, k, 0);
+      if (k >= n_wide) break;
+      const DevInst& I = insts[order[k]];
+      if (lane_id() == 0) ctl->inst = &I;
+      run_walk(I, P.N, P.W, pool, C);
+    }
+    if (lane_id() == 0) ctl->cmd = 0;
+    __syncwarp();
+    bar_sync(1, 32 * nw);  // release the helpers to exit
+  } else {
+    for (;;) {
+      bar_sync(1, 32 * nw);
+      const int cmd = *reinterpret_cast<volatile int*>(&ctl->cmd);
+      if (cmd == 0) break;
+      const DevInst* I = *reinterpret_cast<const DevInst* volatile*>(&ctl->inst);
+      Net& N = P.N;
+      N.ient = I->ient;
+      N.snk = 2 * I->n + 1;
+      N.S = *reinterpret_cast<volatile long long*>(&ctl->S);
+      const int nsrc = *reinterpret_cast<volatile int*>(&ctl->nsrc);
+      int tgt;
+      if (cmd == 2)
+        bfs_core<true, true>(N, nsrc, tgt, C, wi);
+      else
+        bfs_core<false, true>(N, nsrc, tgt, C, wi);
+    }
+  }
   flush_counters(C, ctr);
 }
 
@@ -1482,28 +1596,22 @@ int walk_slots_per_sm(const WsLayout& ws) {
   return blocks * kWarpsPerBlock;
 }
 
-int big_walk_smem_bytes() {
-  int dev = 0, optin = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  return optin;
-}
-
-// d_counter[0] = walker queue cursor, d_counter[1] = resident big CTAs.
+// d_counter[0] = walker queue cursor, d_counter[1] = wide queue cursor.
 int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
                  char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
-                 DeltaPool pool, int32_t n_big, void* stream, void* stream_big) {
-  if (n_big > 0) {
-    const int sm_big = big_walk_smem_bytes();
-    set_smem(walk_kernel_big, sm_big);
-    walk_kernel_big<<<n_big, 32, sm_big, static_cast<cudaStream_t>(stream_big)>>>(
-        d_insts, d_order, d_ws, ws, d_counters, pool, d_counter + 1);
+                 DeltaPool pool, int32_t n_wide, int32_t wide_ctas, int32_t wide_warps, void* stream,
+                 void* stream_wide) {
+  if (n_wide > 0 && wide_ctas > 0) {
+    const size_t sm = static_cast<size_t>(wide_warps) * (128 + 8 * kMaxEnds + ws.smem_bytes) + 128;
+    set_smem(walk_kernel_wide, sm);
+    walk_kernel_wide<<<wide_ctas, 32 * wide_warps, sm, static_cast<cudaStream_t>(stream_wide)>>>(
+        d_insts, n_wide, d_order, d_counter, d_ws, ws, d_counters, pool);
   }
-  if (n_inst > n_big) {
+  if (n_inst > n_wide) {
     const size_t sm = block_smem(ws);
     set_smem(walk_kernel, sm);
     walk_kernel<<<blocks_for(slots), kBlock, sm, static_cast<cudaStream_t>(stream)>>>(
-        d_insts, n_inst, d_order, d_counter, d_ws, ws, slots, d_counters, pool, n_big);
+        d_insts, n_inst, d_order, d_counter, d_ws, ws, slots, d_counters, pool, n_wide, wide_ctas);
   }
   return static_cast<int>(cudaGetLastError());
 }

@@ -69,6 +69,25 @@ def test_every_golden_walk_in_one_batch(walks):
         check_walk_against(b, k, walks[spec], model.blocking_watts, model.quantum_us, full=spec != "config:2")
 
 
+@pytest.mark.parametrize("warps", [2, 4])
+def test_golden_walks_through_the_cooperative_bfs(walks, monkeypatch, warps):
+    """The same 126 walks with every instance on the wide (multi-warp BFS)
+    kernel, and with the wide kernel sharing the batch with the walker."""
+    monkeypatch.setenv("PB_WIDE_WARPS", str(warps))
+    monkeypatch.setenv("PB_WIDE_CTAS", "7")
+    for wide in ("100000", "9"):
+        monkeypatch.setenv("PB_WIDE", wide)
+        b = pb.FrontierBatch()
+        meta = []
+        for spec, w in walks.items():
+            dag, model, tau = instance_from_golden(w)
+            b.add(dag, model, tau)
+            meta.append((spec, model))
+        b.run(0)
+        for k, (spec, model) in enumerate(meta):
+            check_walk_against(b, k, walks[spec], model.blocking_watts, model.quantum_us, full=False)
+
+
 def test_config2_every_point_bit_exact(walks):
     w = walks["config:2"]
     dag, model, tau = instance_from_golden(w)
