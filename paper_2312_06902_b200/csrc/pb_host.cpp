@@ -205,6 +205,18 @@ pb_status validate_and_derive(HostInst& h) {
       sv[u].push_back(v);
     }
   }
+  if (n >= (1 << 24)) return fail(PB_ERR_UNSUPPORTED, "more than 2^24 computations");
+  // level of each internal id (level-major order)
+  std::vector<int32_t> ilev(n);
+  for (int32_t l = 0; l < L; ++l)
+    for (int32_t i = h.lvl_off[l]; i < h.lvl_off[l + 1]; ++i) ilev[i] = l;
+  // sweep ring slot of neighbour u seen from i (pb_internal.h kRingLevels)
+  auto ring = [&](int32_t i, int32_t u) {
+    const int32_t gap = std::abs(ilev[i] - ilev[u]);
+    const int32_t idx = u - h.lvl_off[ilev[u]];
+    if (gap < 1 || gap >= pb::kRingLevels || idx >= 16) return u | (pb::kRingNone << 24);
+    return u | (((ilev[u] % pb::kRingLevels) * 16 + idx) << 24);
+  };
   auto csr = [&](std::vector<std::vector<int32_t>>& lists, std::vector<int32_t>& off,
                  std::vector<int32_t>& idx, std::vector<pb::int4h>& row, bool with_sink) {
     off.assign(n + 1, 0);
@@ -214,9 +226,9 @@ pb_status validate_and_derive(HostInst& h) {
       const auto& l = lists[i];
       const int32_t c = static_cast<int32_t>(l.size());
       row[i].x = std::min(c, 0xffff) | (with_sink && (h.cflag[i] & 2) ? (1 << 16) : 0);
-      if (c > 0) row[i].y = l[0];
-      if (c > 1) row[i].z = l[1];
-      if (c > 2) row[i].w = l[2];
+      if (c > 0) row[i].y = ring(i, l[0]);
+      if (c > 1) row[i].z = ring(i, l[1]);
+      if (c > 2) row[i].w = ring(i, l[2]);
       idx.insert(idx.end(), l.begin(), l.end());
       off[i + 1] = static_cast<int32_t>(idx.size());
     }

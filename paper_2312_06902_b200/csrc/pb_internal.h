@@ -89,8 +89,8 @@ struct DevInst {
   const int32_t* comp_class;  // [n]
   const uint8_t* cflag;       // [n] bit 1: has an edge to the sink
   const int32_t* lvl_off;     // [n_levels + 1]
-  const int4* frow;           // [n] {count | has-sink << 16, first 3 predecessors}
-  const int4* brow;           // [n] {count, first 3 successors}
+  const int4* frow;           // [n] {count | has-sink << 16, first 3 predecessors (u | ring slot << 24)}
+  const int4* brow;           // [n] {count, first 3 successors (same packing)}
   const int32_t* pin_off;     // [n + 1] computation predecessors
   const int32_t* pin;
   const int32_t* pout_off;    // [n + 1] computation successors
@@ -136,6 +136,11 @@ enum : int {
 
 // Shared memory per walker warp: visited bitset + ping-pong frontier.
 constexpr int kFrontCap = 128;  // frontier entries per buffer kept in smem
+// Longest-path sweep: values of the last kRingLevels levels (<= 16 per level)
+// also live in a shared-memory ring per direction; a row-record neighbour is
+// u | slot << 24 with slot = ring slot, or kRingNone to read global memory.
+constexpr int kRingLevels = 4;
+constexpr int kRingNone = 255;
 
 // Per-warp global workspace; arrays sized for the largest instance of a batch.
 // The flow (encoded in resid) persists across the steps of a walk.
@@ -195,8 +200,9 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   L.off_path = take(4 * max_v);
   L.stride = o;
   const int64_t bitwords = (max_v + 31) / 32;
-  // frontier, visited bitset, partner-ok bitset
-  L.smem_bytes = static_cast<int32_t>(16 * 2 * kFrontCap + 2 * align_up(4 * bitwords, 16));
+  // frontier, visited bitset, partner-ok bitset, sweep rings (fwd, bwd)
+  L.smem_bytes = static_cast<int32_t>(16 * 2 * kFrontCap + 2 * align_up(4 * bitwords, 16) +
+                                      2 * kRingLevels * 16 * 16);
   return L;
 }
 

@@ -137,6 +137,7 @@ struct Net {
   uint32_t s_bits;  // smem (shared-window address) visited bitset
   uint32_t s_pok;   // smem bitset: node x < 2n whose computation arc to x ^ 1 has residual > 0
   uint32_t s_fs;    // smem frontier, 2 buffers of kFrontCap int4 entries
+  uint32_t s_ring;  // smem longest-path rings (forward, backward)
   int2* ends;       // smem: phase-B arcs into the sink {position, parent log index}
   int32_t* path;
   int32_t* touch;
@@ -625,6 +626,21 @@ struct Walk {
   int32_t* delta;
 };
 
+__device__ __forceinline__ void sts_ll2(uint32_t a, long long x, long long y) {
+  asm volatile("st.shared.v2.s64 [%0], {%1, %2};" ::"r"(a), "l"(x), "l"(y) : "memory");
+}
+__device__ __forceinline__ longlong2 lds_ll2(uint32_t a) {
+  longlong2 v;
+  asm volatile("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a) : "memory");
+  return v;
+}
+// Neighbour value for the sweep: shared ring slot when the row record has
+// one (neighbour at most kRingLevels - 1 levels away), else global memory.
+__device__ __forceinline__ longlong2 sweep_val(const longlong2* vals, uint32_t ring, int packed) {
+  const unsigned slot = static_cast<unsigned>(packed) >> 24;
+  return slot != kRingNone ? lds_ll2(ring + 16u * slot) : vals[packed & 0xffffff];
+}
+
 // Fused longest path over the level-major order (K2).  Forward lanes (0-15)
 // compute fin[i] = max over predecessors of fin + (dp[i], dr[i]); backward
 // lanes (16-31, when `back`) compute tl[i].x = dp[i] + max over successors
@@ -632,7 +648,8 @@ struct Walk {
 // in the same iteration.  The per-level static data (row records, level
 // bounds) and the durations are loaded one iteration ahead.
 __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr, longlong2* fin,
-                      longlong2* tl, bool back, long long& msp, long long& msr, Counters& C) {
+                      longlong2* tl, bool back, long long& msp, long long& msr, uint32_t s_ring,
+                      Counters& C) {
   const int ln = lane_id();
   const long long t0 = now();
   const bool fwd = ln < 16;
@@ -643,6 +660,7 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
   const int32_t* noff = fwd ? I.pin_off : I.pout_off;
   const int32_t* nb = fwd ? I.pin : I.pout;
   longlong2* vals = fwd ? fin : tl;
+  const uint32_t ring = (fwd ? s_ring : s_ring + 16u * kRingLevels * 16);
   long long mp = 0, mr = 0;
   C.add(kPrLpLevels, L);
   auto lev_of = [&](int k) { return fwd ? k : L - 1 - k; };
@@ -681,9 +699,9 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
       const int cnt = r0.x & 0xffff;
       long long x = 0, y = 0;
       longlong2 v0 = make_longlong2(0, 0), v1 = v0, v2 = v0;
-      if (cnt > 0) v0 = vals[r0.y];
-      if (cnt > 1) v1 = vals[r0.z];
-      if (cnt > 2) v2 = vals[r0.w];
+      if (cnt > 0) v0 = sweep_val(vals, ring, r0.y);
+      if (cnt > 1) v1 = sweep_val(vals, ring, r0.z);
+      if (cnt > 2) v2 = sweep_val(vals, ring, r0.w);
       x = max(max(v0.x, v1.x), max(v2.x, x));
       y = max(max(v0.y, v1.y), max(v2.y, y));
       if (cnt > 3)
@@ -694,6 +712,7 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
         }
       const long long a = x + dp0, c = fwd ? y + dr0 : 0;
       vals[i0] = make_longlong2(a, c);
+      if (s < 16) sts_ll2(ring + 16u * ((lev_of(k) % kRingLevels) * 16 + s), a, c);
       if (fwd && (r0.x >> 16)) {
         mp = max(mp, a);
         mr = max(mr, c);
@@ -714,6 +733,16 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
           mr = max(mr, cc);
         }
         ++C.comp_visits;
+      }
+    }
+    // sliding-window L1 prefetch of the rows and durations a few levels
+    // ahead (level-major order: they are contiguous)
+    if (active && b0 < e0) {
+      const int ahead = fwd ? b0 + 32 + 8 * s : b0 - 32 - 8 * s;
+      if (ahead >= 0 && ahead < I.n) {
+        pf_l1(row + ahead);
+        pf_l1(dp + ahead);
+        if (fwd) pf_l1(dr + ahead);
       }
     }
     __syncwarp();
@@ -814,19 +843,15 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
     long long t[kU], fx[kU], tx[kU];
     bool oc[kU];
     uint8_t dt[kU];
+    // branch-free, clamped loads: all 5 x kU requests are in flight together
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const int i = base + 32 * q + ln;
-      t[q] = fx[q] = tx[q] = 0;
-      oc[q] = false;
-      dt[q] = 0;
-      if (i < n) {
-        t[q] = W.durp[i];
-        fx[q] = W.fin[i].x;
-        tx[q] = W.tl[i].x;
-        oc[q] = W.ecrit[i];
-        dt[q] = W.dirty[i];
-      }
+      const int i = min(base + 32 * q + ln, n - 1);
+      t[q] = W.durp[i];
+      fx[q] = W.fin[i].x;
+      tx[q] = W.tl[i].x;
+      oc[q] = W.ecrit[i];
+      dt[q] = W.dirty[i];
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
@@ -909,29 +934,22 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
     long long te[kU], he[kU], hd[kU];
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const int j = base + 32 * q + ln;
-      uv[q] = make_int2(n, n + 1);
-      oc[q] = false;
-      if (j < I.ne) {
-        uv[q] = I.dep_nd[j];
-        oc[q] = W.ecrit[n + j];
-      }
+      const int j = min(base + 32 * q + ln, I.ne - 1);
+      uv[q] = I.dep_nd[j];
+      oc[q] = W.ecrit[n + j];
     }
+    // endpoint loads, branch-free (index 0 stands in for the source / sink)
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      tc[q] = hc[q] = true;
-      te[q] = 0;
-      he[q] = ms;
-      hd[q] = 0;
-      if (uv[q].x != n) {
-        tc[q] = W.ecrit[uv[q].x];
-        te[q] = W.fin[uv[q].x].x;
-      }
-      if (uv[q].y != n + 1) {
-        hc[q] = W.ecrit[uv[q].y];
-        he[q] = W.fin[uv[q].y].x;
-        hd[q] = W.durp[uv[q].y];
-      }
+      const bool ts = uv[q].x == n, hs = uv[q].y == n + 1;
+      const int tu = ts ? 0 : uv[q].x, hv = hs ? 0 : uv[q].y;
+      const bool tcr = W.ecrit[tu], hcr = W.ecrit[hv];
+      const long long tf = W.fin[tu].x, hf = W.fin[hv].x, hdd = W.durp[hv];
+      tc[q] = ts || tcr;
+      hc[q] = hs || hcr;
+      te[q] = ts ? 0 : tf;
+      he[q] = hs ? ms : hf;
+      hd[q] = hs ? 0 : hdd;
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
@@ -1054,7 +1072,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   for (int i = ln; i < n; i += 32) W.durr[i] = I.pt_time[I.cls_pt_off[I.comp_class[i]]];
   __syncwarp();
   long long t_min, unused;
-  sweep(I, W.durr, W.durr, W.fin, W.tl, false, t_min, unused, C);
+  sweep(I, W.durr, W.durr, W.fin, W.tl, false, t_min, unused, N.s_ring, C);
   for (int i = ln; i < n; i += 32) {
     const int c = I.comp_class[i];
     long long t;
@@ -1079,7 +1097,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
 
   const long long t_walk0 = now();
   long long t_cur, t_real;
-  sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_cur, t_real, C);
+  sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_cur, t_real, N.s_ring, C);
   const long long t_star = t_cur;
   if (ln == 0) write_point(I, 0, t_cur, t_real, spe, spt, sre, srt, 0, 0, 0, 0, 0);
   int steps = 0;
@@ -1223,7 +1241,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     // refresh_totals (frontier.hpp:64-67) + discretize (frontier.hpp:157):
     // planned and realized makespans and the next step's tails, one sweep
     long long t_new;
-    sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_new, t_real, C);
+    sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_new, t_real, N.s_ring, C);
     if (I.mode == kModeDiscover && t_new >= t_cur) {
       stop = PB_STOP_NO_PROGRESS;
       break;
@@ -1286,6 +1304,7 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.N.s_fs = sa + 8 * kMaxEnds;
   p.N.s_bits = sa + 8 * kMaxEnds + 16 * 2 * kFrontCap;
   p.N.s_pok = p.N.s_bits + static_cast<uint32_t>((4 * ((L.max_v + 31) / 32) + 15) / 16 * 16);
+  p.N.s_ring = p.N.s_pok + static_cast<uint32_t>((4 * ((L.max_v + 31) / 32) + 15) / 16 * 16);
   p.N.ctl = nullptr;
   p.N.nw = 1;
   return p;
@@ -1525,7 +1544,7 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
     for (int i = ln; i < n; i += 32) W.durp[i] = O.dur[I.orig[i]];
     __syncwarp();
     long long ms, unused;
-    sweep(I, W.durp, W.durp, W.fin, W.tl, true, ms, unused, C);
+    sweep(I, W.durp, W.durp, W.fin, W.tl, true, ms, unused, P.N.s_ring, C);
     __syncwarp();
     // latest of the source node: min over its successors' latest start
     long long ls = ms;
