@@ -680,6 +680,7 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
     dp0 = dp[b0 + s];
     dr0 = fwd ? dr[b0 + s] : 0;
   }
+  int pf = fwd ? 0 : I.n;  // next row not yet prefetched (this half's direction)
   for (int k = 0; k < L; ++k) {
     // issue the loads of the next iterations
     int b2 = 0, e2 = 0;
@@ -735,14 +736,30 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
         ++C.comp_visits;
       }
     }
-    // sliding-window L1 prefetch of the rows and durations a few levels
-    // ahead (level-major order: they are contiguous)
-    if (active && b0 < e0) {
-      const int ahead = fwd ? b0 + 32 + 8 * s : b0 - 32 - 8 * s;
-      if (ahead >= 0 && ahead < I.n) {
-        pf_l1(row + ahead);
-        pf_l1(dp + ahead);
-        if (fwd) pf_l1(dr + ahead);
+    // each row / duration line prefetched once, ~64 computations ahead
+    // (level-major order: the sweep consumes them contiguously)
+    if (active) {
+      if (fwd) {
+        const int want = min(b0 + 64, I.n);
+        if (pf < want) {
+          const int r = pf + 8 * s;
+          if (r < want) {
+            pf_l1(row + r);
+            pf_l1(dp + r);
+            pf_l1(dr + r);
+          }
+          pf = min(want, pf + 128);
+        }
+      } else {
+        const int want = max(b0 - 64, 0);
+        if (pf > want) {
+          const int r = pf - 8 * (s + 1);
+          if (r >= want) {
+            pf_l1(row + r);
+            pf_l1(dp + r);
+          }
+          pf = max(want, pf - 128);
+        }
       }
     }
     __syncwarp();
