@@ -188,6 +188,30 @@ pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out);
 pb_status pb_batch_profile(const pb_batch* b, int64_t* out, int32_t n);
 void pb_batch_destroy(pb_batch* b);
 
+/* ---- straggler sweep on the device-resident frontiers -- */
+/* Savings over a cluster of `pipelines` identical pipelines when one
+ * straggles to T' = llround(factor * T_min): the P-1 healthy pipelines move
+ * from all-max to lookup(frontier, T') (straggler_savings, baselines.hpp:
+ * 162-188; lookup, frontier.hpp:212-220; Eq. 3 energy_report,
+ * emulator.hpp:77-112 with the blocking power and quantum of the instance).
+ * One device thread per (instance, factor) on the frontier points of the
+ * last single-device pb_batch_run.  Energies agree with the reference to
+ * 1e-9 relative (the per-stage blocking terms are summed as one product). */
+typedef struct {
+  double factor;
+  double savings_pct;
+  double savings_mj;
+  double all_max_mj; /* energy_report(all-max).total_mj */
+  double tuned_mj;   /* energy_report(frontier point).total_mj */
+  int32_t point;     /* index of the looked-up frontier point */
+  int32_t status;    /* PB_OK, or PB_ERR_INVALID_ARGUMENT when T' is shorter
+                        than that point's realized iteration (emulator.hpp:85) */
+} pb_savings_row;
+/* out[k * n_factors + j] for instance k and factors[j]; num_stages[k] is
+ * NodeDag::num_stages of instance k. */
+pb_status pb_batch_straggler(pb_batch* b, int32_t n_factors, const double* factors, int32_t pipelines,
+                             const int32_t* num_stages, pb_savings_row* out);
+
 /* ---- component kernels, exposed for parity tests ----------------------- */
 /* annotate_slack (dag.hpp:233-286) for a batch of DAGs on one device.
  * Per DAG g: n[g] computations, ne[g] node-DAG edges; arrays concatenated;

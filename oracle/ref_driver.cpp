@@ -15,6 +15,9 @@
 //   bench <threads> <spec>...  wall-time of discover_frontier over a thread
 //                            pool (one instance per task, LPT order given)
 //   fit <spec>               CostModel curves (bit patterns) of an instance
+//   savings <P> <factors,...> <spec>...
+//                            straggler_savings (baselines.hpp:162-188) on the
+//                            reference frontier: rows + the looked-up point
 //
 // Instance specs
 //   g9:N:M:B:imbalance:seed:straggler:phi     SURVEY §8d generator
@@ -501,6 +504,35 @@ int mode_bench(int argc, char** argv) {
 // reference's public API (the discover_frontier loop, frontier.hpp:166-189)
 // until it reaches T_min or its per-instance budget expires; instances run
 // one per thread.  Frontier points = schedules produced (seed included).
+// straggler_savings over a P-pipeline cluster for comma-separated factors.
+int mode_savings(int argc, char** argv) {
+  ClusterScenario sc;
+  sc.pipelines = std::stoi(argv[2]);
+  std::vector<double> factors;
+  for (const auto& f : split(argv[3], ',')) factors.push_back(std::stod(f));
+  for (int i = 4; i < argc; ++i) {
+    const Instance in = make_instance(argv[i]);
+    const Frontier fr = discover_frontier(in.dag, in.model, in.tau);
+    const auto rows = straggler_savings(fr, in.dag, in.model, sc, factors);
+    const AllMaxAssignment am = all_max_assignment(in.dag, in.model);
+    const Quanta tmin = simulate(in.dag, am.durations).iteration_time;
+    std::ostringstream o;
+    o << "{\"spec\":\"" << argv[i] << "\",\"pipelines\":" << sc.pipelines << ",\"num_stages\":" << in.dag.num_stages
+      << ",\"rows\":[";
+    for (size_t k = 0; k < rows.size(); ++k) {
+      const Quanta tp = std::llround(factors[k] * static_cast<double>(tmin));
+      const EnergySchedule& s = lookup(fr, tp);
+      char buf[256];
+      std::snprintf(buf, sizeof buf, "%s{\"factor\":%.17g,\"savings_pct\":%.17g,\"savings_mj\":%.17g,\"point\":%d}",
+                    k ? "," : "", rows[k].factor, rows[k].savings_pct, rows[k].savings_mj, s.schedule_id);
+      o << buf;
+    }
+    o << "]}";
+    std::printf("%s\n", o.str().c_str());
+  }
+  return 0;
+}
+
 int mode_budget(int argc, char** argv) {
   const double budget = std::stod(argv[2]);
   const int threads = std::max(1, std::stoi(argv[3]));
@@ -573,6 +605,7 @@ int main(int argc, char** argv) {
     if (mode == "slack") return mode_slack(argc, argv);
     if (mode == "bench") return mode_bench(argc, argv);
     if (mode == "budget") return mode_budget(argc, argv);
+    if (mode == "savings") return mode_savings(argc, argv);
     if (mode == "fit") {
       for (int i = 2; i < argc; ++i) {
         const Instance in = make_instance(argv[i]);

@@ -130,6 +130,18 @@ class RunStats(C.Structure):
     ]
 
 
+class SavingsRow(C.Structure):
+    _fields_ = [
+        ("factor", C.c_double),
+        ("savings_pct", C.c_double),
+        ("savings_mj", C.c_double),
+        ("all_max_mj", C.c_double),
+        ("tuned_mj", C.c_double),
+        ("point", C.c_int32),
+        ("status", C.c_int32),
+    ]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -156,6 +168,7 @@ def _load() -> C.CDLL:
         "pb_batch_schedule": (C.c_int, [P, C.c_int32, C.c_int32, i64p, i64p, i32p, i64p, i64p, f64p, f64p]),
         "pb_batch_stats": (C.c_int, [P, C.POINTER(RunStats)]),
         "pb_batch_profile": (C.c_int, [P, i64p, C.c_int32]),
+        "pb_batch_straggler": (C.c_int, [P, C.c_int32, f64p, C.c_int32, i32p, C.POINTER(SavingsRow)]),
         "pb_batch_destroy": (None, [P]),
         "pb_annotate_slack_batch": (C.c_int, [C.c_int32, C.c_int32, i32p, i32p, i32p, i32p, i64p,
                                               i64p, i64p, u8p, i64p]),
@@ -183,7 +196,7 @@ EXPORTED = (
     "pb_batch_run", "pb_batch_prepare", "pb_batch_launch", "pb_batch_fetch", "pb_batch_size",
     "pb_batch_run_multi", "pb_batch_summary", "pb_batch_points", "pb_batch_deltas", "pb_batch_schedule",
     "pb_batch_stats", "pb_batch_profile", "pb_batch_destroy", "pb_annotate_slack_batch", "pb_flow_min_cut_batch",
-    "pb_g9_stage_bases", "pb_g9_batch_params", "pb_g9_profile", "pb_batch_add_g9",
+    "pb_g9_stage_bases", "pb_g9_batch_params", "pb_g9_profile", "pb_batch_add_g9", "pb_batch_straggler",
 )
 
 

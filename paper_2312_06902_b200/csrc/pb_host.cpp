@@ -1138,6 +1138,61 @@ pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out) {
   return PB_OK;
 }
 
+// ------------------------------------------------------- straggler sweep
+
+pb_status pb_batch_straggler(pb_batch* b, int32_t n_factors, const double* factors, int32_t pipelines,
+                             const int32_t* num_stages, pb_savings_row* out) {
+  if (!b || n_factors < 0 || (n_factors && (!factors || !out)) || !num_stages)
+    return fail(PB_ERR_INVALID_ARGUMENT, "null argument");
+  if (pipelines < 1) return fail(PB_ERR_INVALID_ARGUMENT, "need at least one pipeline");
+  for (int32_t j = 0; j < n_factors; ++j)
+    if (!(factors[j] >= 1.0)) return fail(PB_ERR_INVALID_ARGUMENT, "straggler factor must be >= 1");
+  if (!b->have_results || b->run.device < 0)
+    return fail(PB_ERR_LOGIC, "pb_batch_run the batch on one device first");
+  const int32_t N = static_cast<int32_t>(b->insts.size());
+  if (N == 0 || n_factors == 0) return PB_OK;
+  return guarded([&]() -> pb_status {
+    DeviceRun& R = b->run;
+    ck(cudaSetDevice(R.device), "cudaSetDevice");
+    std::vector<pb::DevStraggler> jobs(N);
+    for (int32_t k = 0; k < N; ++k) {
+      const HostInst& h = b->insts[k];
+      pb::DevStraggler& J = jobs[k];
+      J.points = reinterpret_cast<const pb_point*>(R.d_out + b->out_points[k]);
+      J.summary = reinterpret_cast<const pb_frontier_summary*>(R.d_out + b->out_summary[k]);
+      J.am_energy = 0;
+      J.am_time = 0;
+      for (int32_t i = 0; i < h.n; ++i) {  // all_max_assignment (emulator.hpp:140-149)
+        const int32_t p0 = h.cls_pt_off[h.comp_class[i]];
+        J.am_energy += h.pt_energy[p0];
+        J.am_time += h.pt_time[p0];
+      }
+      J.watts = h.watts;
+      J.quantum = h.quantum;
+      J.stages = num_stages[k];
+      J.pad = 0;
+      if (num_stages[k] < 1) return fail(PB_ERR_INVALID_ARGUMENT, "num_stages must be positive");
+    }
+    pb::DevStraggler* d_jobs = nullptr;
+    double* d_f = nullptr;
+    pb_savings_row* d_out = nullptr;
+    const size_t rows = static_cast<size_t>(N) * n_factors;
+    ck(cudaMalloc(&d_jobs, sizeof(pb::DevStraggler) * N), "malloc");
+    ck(cudaMalloc(&d_f, sizeof(double) * n_factors), "malloc");
+    ck(cudaMalloc(&d_out, sizeof(pb_savings_row) * rows), "malloc");
+    ck(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(pb::DevStraggler) * N, cudaMemcpyHostToDevice, R.stream), "H2D");
+    ck(cudaMemcpyAsync(d_f, factors, sizeof(double) * n_factors, cudaMemcpyHostToDevice, R.stream), "H2D");
+    const int rc = pb::launch_straggler(d_jobs, N, d_f, n_factors, pipelines, d_out, R.stream);
+    if (rc) throw CudaError(cudaGetErrorString(static_cast<cudaError_t>(rc)));
+    ck(cudaMemcpyAsync(out, d_out, sizeof(pb_savings_row) * rows, cudaMemcpyDeviceToHost, R.stream), "D2H");
+    ck(cudaStreamSynchronize(R.stream), "straggler kernel");
+    cudaFree(d_jobs);
+    cudaFree(d_f);
+    cudaFree(d_out);
+    return PB_OK;
+  });
+}
+
 // ------------------------------------------------------- component kernels
 
 pb_status pb_annotate_slack_batch(int32_t device, int32_t count, const int32_t* n, const int32_t* ne,

@@ -237,6 +237,18 @@ struct SlackOut {
   uint8_t* critical;
 };
 
+// Straggler-sweep job of one instance (pb_batch_straggler).
+struct DevStraggler {
+  const pb_point* points;
+  const pb_frontier_summary* summary;
+  int64_t am_energy, am_time;  // all-max sums of energy (mJ) and duration (quanta)
+  double watts;
+  int64_t quantum;
+  int32_t stages, pad;
+};
+int launch_straggler(const DevStraggler* d_jobs, int32_t n_inst, const double* d_factors, int32_t n_factors,
+                     int32_t pipelines, pb_savings_row* d_out, void* stream);
+
 // Host-side launchers (pb_kernels.cu).  slots = number of walker warps (one
 // workspace each).
 // The first n_wide instances of the LPT order (the longest walks, which

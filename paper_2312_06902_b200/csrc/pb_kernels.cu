@@ -1428,6 +1428,56 @@ __global__ void __launch_bounds__(kBlock) walk_kernel_wide(const DevInst* insts,
   flush_counters(C, ctr);
 }
 
+// ------------------------------------------------------- straggler sweep
+
+// blocking_energy_mj (units.hpp:38-41)
+__device__ __forceinline__ double blocking_mj(double w, long long t, long long q) {
+  return w * static_cast<double>(t) * static_cast<double>(q) * 1e-3;
+}
+
+// energy_report(...).total_mj (emulator.hpp:77-112): computation energy +
+// per-stage blocking over the iteration + per-stage straggler wait.
+__device__ __forceinline__ double report_total(double w, long long q, int stages, long long e_sum, long long t,
+                                               long long busy_sum, long long t_prime) {
+  return static_cast<double>(e_sum) + blocking_mj(w, static_cast<long long>(stages) * t - busy_sum, q) +
+         static_cast<double>(stages) * blocking_mj(w, t_prime - t, q);
+}
+
+// One thread per (instance, factor): straggler_savings (baselines.hpp:162-188).
+__global__ void straggler_kernel(const DevStraggler* jobs, int n_inst, const double* factors, int n_factors,
+                                 int pipelines, pb_savings_row* out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_inst * n_factors) return;
+  const int k = g / n_factors, j = g - k * n_factors;
+  const DevStraggler J = jobs[k];
+  const pb_frontier_summary sm = *J.summary;
+  const double f = factors[j];
+  const long long tp = llround(f * static_cast<double>(sm.t_min));
+  pb_savings_row r;
+  r.factor = f;
+  r.status = PB_OK;
+  r.all_max_mj = report_total(J.watts, J.quantum, J.stages, J.am_energy, sm.t_min, J.am_time, tp);
+  // lookup (frontier.hpp:212-220): first point, in decreasing planned time,
+  // with t_planned <= min(T*, T'); the last point if none
+  const long long target = sm.t_star < tp ? sm.t_star : tp;
+  int lo = 0, hi = sm.steps + 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (J.points[mid].t_planned > target)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  if (lo > sm.steps) lo = sm.steps;
+  const pb_point p = J.points[lo];
+  r.point = lo;
+  if (tp < p.t_realized) r.status = PB_ERR_INVALID_ARGUMENT;
+  r.tuned_mj = report_total(J.watts, J.quantum, J.stages, p.sum_realized_e, p.t_realized, p.sum_realized_t, tp);
+  r.savings_mj = static_cast<double>(pipelines - 1) * (r.all_max_mj - r.tuned_mj);
+  r.savings_pct = 100.0 * r.savings_mj / (static_cast<double>(pipelines) * r.all_max_mj);
+  out[g] = r;
+}
+
 // ------------------------------------------------------------ flow jobs
 
 // max_flow_lower_bounds + min_cut_from_flow on an arbitrary FlowGraph with
@@ -1649,6 +1699,14 @@ int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order,
     walk_kernel<<<blocks_for(slots), kBlock, sm, static_cast<cudaStream_t>(stream)>>>(
         d_insts, n_inst, d_order, d_counter, d_ws, ws, slots, d_counters, pool, n_wide, wide_ctas);
   }
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_straggler(const DevStraggler* d_jobs, int32_t n_inst, const double* d_factors, int32_t n_factors,
+                     int32_t pipelines, pb_savings_row* d_out, void* stream) {
+  const int total = n_inst * n_factors;
+  straggler_kernel<<<(total + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_jobs, n_inst, d_factors,
+                                                                                      n_factors, pipelines, d_out);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -133,6 +133,16 @@ class FrontierBatch:
         N.check(N.lib.pb_batch_stats(self._h, C.byref(s)))
         return s
 
+    def straggler(self, factors, pipelines: int, num_stages) -> np.ndarray:
+        """straggler_savings (baselines.hpp:162-188) of every instance on the
+        device-resident frontiers of the last run: rows[k, j] for factors[j]."""
+        f = np.ascontiguousarray(factors, np.float64)
+        st = np.ascontiguousarray(num_stages, np.int32)
+        buf = (N.SavingsRow * (len(self) * len(f)))()
+        N.check(N.lib.pb_batch_straggler(self._h, len(f), N.ptr(f, C.c_double), pipelines,
+                                         N.ptr(st, C.c_int32), buf))
+        return np.ctypeslib.as_array(buf).copy().reshape(len(self), len(f))
+
     # -- results
     def summary(self, k: int) -> N.FrontierSummary:
         s = N.FrontierSummary()

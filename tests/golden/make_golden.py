@@ -13,6 +13,10 @@ Fixtures (JSON lines, gzip):
                       seed 424242, <= 12 nodes (acceptance.cpp:137-157)
   flow7302.jsonl.gz   test_flow.cpp:90-114 corpus: 600 graphs, seed 7302
   slack7102.jsonl.gz  annotate_slack on random DAGs (test_dag.cpp:244-263 style)
+  savings.jsonl.gz    straggler_savings rows (baselines.hpp:162-188) on the
+                      reference frontier, 8 pipelines, the config-4 factor sweep
+
+    python tests/golden/make_golden.py [walks|flow|slack|savings ...]
   batch_small.jsonl.gz  small config-5 style G9 instances (summaries only)
 """
 import gzip
@@ -39,19 +43,30 @@ def write(name, lines):
     print(f"{name}: {len(lines)} records, {os.path.getsize(path)} bytes")
 
 
+SAVINGS_FACTORS = "1.0,1.05,1.1,1.2,1.3,1.5"  # SURVEY §8d config-4 straggler sweep
+
+
 def main():
     if not os.path.exists(DRIVER):
         sys.exit("build the reference driver first: make -C oracle ref")
+    parts = set(sys.argv[1:]) or {"walks", "flow", "slack", "savings"}
     walk_specs = ["diamond", "lone:1000:9000:3000:5000", "lone:1000:9000:3000:5000:800",
                   "lone:1000:5000:11000:800", "config:1", "config:2"]
     walk_specs += [f"grid:{s}:{1 + s % 3}:{1 + s % 4}" for s in range(1, 41)]
     walk_specs += [f"grid:{s}:{2 + s % 3}:{2 + s % 5}:4" for s in range(100, 120)]
     walk_specs += [f"cubic:{s}:{1 + s % 4}:{1 + s % 6}" for s in range(1, 41)]
     walk_specs += [f"g9:{2 + s % 5}:{2 + s % 7}:{8 + s % 4}:1.2:{s}:{s % 3 - 1}:1.5" for s in range(1, 21)]
-    write("walks.jsonl.gz", run("walkcheck", *walk_specs))
-    write("flow424242.jsonl.gz", run("flow", "424242", "1000", "12", "30"))
-    write("flow7302.jsonl.gz", run("flow", "7302", "600", "8", "30"))
-    write("slack7102.jsonl.gz", run("slack", "7102", "200"))
+    if "walks" in parts:
+        write("walks.jsonl.gz", run("walkcheck", *walk_specs))
+    if "flow" in parts:
+        write("flow424242.jsonl.gz", run("flow", "424242", "1000", "12", "30"))
+        write("flow7302.jsonl.gz", run("flow", "7302", "600", "8", "30"))
+    if "slack" in parts:
+        write("slack7102.jsonl.gz", run("slack", "7102", "200"))
+    if "savings" in parts:
+        sav = [w for w in walk_specs if not w.startswith("cubic")]  # cubic walks stop early (infeasible)
+        sav += [f"g9:4:{8 + s}:10:1.1:{s}:{s % 4}:{[1.0, 1.1, 1.3, 1.5][s % 4]}" for s in range(6)]
+        write("savings.jsonl.gz", run("savings", "8", SAVINGS_FACTORS, *sav))
 
 
 if __name__ == "__main__":

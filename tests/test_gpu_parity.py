@@ -275,3 +275,34 @@ def test_full_size_walk_properties(cfg, phi):
     last = b.schedule(0, s.steps)
     assert sum(last.planned_t) == pts["sum_planned_t"][-1]
     assert sum(last.realized_e) == pts["sum_realized_e"][-1]
+
+
+def test_straggler_sweep_matches_reference(walks):
+    """pb_batch_straggler (device lookup + Eq. 3 energy) against the unmodified
+    reference's straggler_savings on its own frontier (tests/golden/savings):
+    the looked-up point is identical; energies within 1e-9 relative to the
+    all-max energy (the reference sums per-stage blocking terms one by one)."""
+    from conftest import load_golden
+    from fixtures import instance_from_golden
+    recs = load_golden("savings.jsonl.gz")
+    b = pb.FrontierBatch()
+    for r in recs:
+        spec = r["spec"]
+        if spec in walks:
+            dag, model, tau = instance_from_golden(walks[spec])
+            b.add(dag, model, tau)
+        else:  # g9:N:M:B:imb:seed:straggler:phi
+            _, N_, M_, B_, imb, seed, st, phi = spec.split(":")
+            b.add_g9(g9.G9Params(int(N_), int(M_), int(B_), float(imb), int(seed), int(st), float(phi)))
+    b.run(0)
+    factors = [row["factor"] for row in recs[0]["rows"]]
+    P = recs[0]["pipelines"]
+    out = b.straggler(factors, P, [r["num_stages"] for r in recs])
+    for k, r in enumerate(recs):
+        for j, ref in enumerate(r["rows"]):
+            got = out[k, j]
+            assert got["status"] == 0, r["spec"]
+            assert got["point"] == ref["point"], (r["spec"], ref["factor"])
+            scale = (P - 1) * abs(got["all_max_mj"])
+            assert abs(got["savings_mj"] - ref["savings_mj"]) <= 1e-9 * scale, (r["spec"], ref, got)
+            assert abs(got["savings_pct"] - ref["savings_pct"]) <= 1e-9 * 100, (r["spec"], ref, got)
