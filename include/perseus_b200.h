@@ -166,6 +166,14 @@ pb_status pb_batch_deltas(const pb_batch* b, int32_t index, int32_t* ids, uint8_
 pb_status pb_batch_schedule(const pb_batch* b, int32_t index, int32_t k, int64_t* planned_t,
                             int64_t* planned_e, int32_t* freq_mhz, int64_t* realized_t,
                             int64_t* realized_e, double* eff_planned, double* eff_realized);
+/* Optimizer artifacts from the delta log, byte-identical to the reference
+ * writer (serde.hpp:250-257 frontier_csv; write_frontier_artifacts,
+ * serde.hpp:304-316: schedule_json(s).dump(2) + "\n").  *len receives the
+ * byte count; bytes are written when buf != NULL and cap >= *len. */
+pb_status pb_batch_frontier_csv(const pb_batch* b, int32_t index, int64_t quantum_us, char* buf,
+                                int64_t cap, int64_t* len);
+pb_status pb_batch_schedule_json(const pb_batch* b, int32_t index, int32_t k, int64_t quantum_us,
+                                 char* buf, int64_t cap, int64_t* len);
 /* Device-side timing/counters of the last run: kernel ms and work counters
  * (arc scans, node updates, push-relabel rounds). */
 typedef struct {

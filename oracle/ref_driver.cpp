@@ -15,6 +15,10 @@
 //   bench <threads> <spec>...  wall-time of discover_frontier over a thread
 //                            pool (one instance per task, LPT order given)
 //   fit <spec>               CostModel curves (bit patterns) of an instance
+//   artifacts <quantum> <spec>...
+//                            frontier.csv + schedule_<k>.json bytes
+//                            (serde.hpp frontier_csv / schedule_json dump(2))
+//                            for the first, middle and last schedules
 //   savings <P> <factors,...> <spec>...
 //                            straggler_savings (baselines.hpp:162-188) on the
 //                            reference frontier: rows + the looked-up point
@@ -41,6 +45,7 @@
 
 #include "helpers.hpp"  // reference tests: generators + independent oracles
 #include "perseus/frontier.hpp"
+#include "perseus/serde.hpp"
 #include "g9.hpp"
 
 using namespace perseus;
@@ -533,6 +538,24 @@ int mode_savings(int argc, char** argv) {
   return 0;
 }
 
+int mode_artifacts(int argc, char** argv) {
+  const std::int64_t q = std::stoll(argv[2]);
+  for (int i = 3; i < argc; ++i) {
+    const Instance in = make_instance(argv[i]);
+    const Frontier fr = discover_frontier(in.dag, in.model, in.tau);
+    nlohmann::ordered_json j;
+    j["spec"] = argv[i];
+    j["quantum"] = q;
+    j["csv"] = frontier_csv(fr, q);
+    const int last = static_cast<int>(fr.schedules.size()) - 1;
+    nlohmann::ordered_json sj = nlohmann::ordered_json::object();
+    for (int k : {0, last / 2, last}) sj[std::to_string(k)] = schedule_json(fr.schedules[k], q).dump(2) + "\n";
+    j["schedules"] = sj;
+    std::printf("%s\n", j.dump().c_str());
+  }
+  return 0;
+}
+
 int mode_budget(int argc, char** argv) {
   const double budget = std::stod(argv[2]);
   const int threads = std::max(1, std::stoi(argv[3]));
@@ -606,6 +629,7 @@ int main(int argc, char** argv) {
     if (mode == "bench") return mode_bench(argc, argv);
     if (mode == "budget") return mode_budget(argc, argv);
     if (mode == "savings") return mode_savings(argc, argv);
+    if (mode == "artifacts") return mode_artifacts(argc, argv);
     if (mode == "fit") {
       for (int i = 2; i < argc; ++i) {
         const Instance in = make_instance(argv[i]);

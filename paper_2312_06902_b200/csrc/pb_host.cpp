@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <array>
+#include <charconv>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -1060,70 +1062,207 @@ pb_status pb_batch_deltas(const pb_batch* b, int32_t k, int32_t* ids, uint8_t* c
   return PB_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Replays instance k's delta log point by point (caller ids) and
+// materializes EnergySchedule fields (frontier.hpp:20-33) at any point.
+struct Replay {
+  const pb_batch* b;
+  int32_t k;
+  const HostInst& h;
+  const pb_point* pts;
+  const int32_t* ids;
+  const uint8_t* cho;
+  std::vector<int64_t> pt;
+  std::vector<int32_t> ch;
+  int32_t at = 0;
+
+  Replay(const pb_batch* bb, int32_t kk)
+      : b(bb), k(kk), h(bb->insts[kk]),
+        pts(reinterpret_cast<const pb_point*>(bb->out.data() + bb->out_points[kk])),
+        ids(bb->pool_ids.data() + bb->pool_base[kk]), cho(bb->pool_choice.data() + bb->pool_base[kk]) {
+    const int32_t n = h.n;
+    pt.resize(n);
+    ch.resize(n);
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t c = h.comp_class[i];
+      pt[i] = !h.start.empty() ? h.start[i] : (h.cls_const[c] ? h.pt_time[h.cls_pt_off[c]] : h.cls_trange[2 * c + 1]);
+      int32_t chosen = 0;  // discretize (frontier.hpp:146-156)
+      for (int32_t p = h.cls_pt_off[c]; p < h.cls_pt_off[c + 1]; ++p)
+        if (h.pt_time[p] <= pt[i]) chosen = p - h.cls_pt_off[c];
+      ch[i] = chosen;
+    }
+  }
+  void advance_to(int32_t which) {
+    for (; at < which; ++at) {
+      const pb_point& p = pts[at + 1];
+      const int32_t cnt = p.n_sped + p.n_slowed;
+      for (int32_t j = p.id_begin; j < p.id_begin + cnt; ++j) {
+        const int32_t x = ids[j];
+        const int32_t i = (x > 0 ? x : -x) - 1;
+        pt[i] += x > 0 ? -p.step_size : p.step_size;
+        ch[i] = cho[j];
+      }
+    }
+  }
+  int64_t planned_energy(int32_t i) const {  // frontier.hpp:59-62
+    const int32_t c = h.comp_class[i];
+    if (h.cls_const[c]) return h.pt_energy[h.cls_pt_off[c]];
+    const int64_t lo = h.cls_trange[2 * c], hi = h.cls_trange[2 * c + 1], t = pt[i];
+    const double v = (t >= lo && t <= hi) ? b->tables[b->cls_tab[k][c] + (t - lo)]
+                                          : h.cls_curve[3 * c] * std::exp(h.cls_curve[3 * c + 1] * static_cast<double>(t)) +
+                                                h.cls_curve[3 * c + 2];
+    return static_cast<int64_t>(std::llround(v));
+  }
+  // effective_total (frontier.hpp:51-57; units.hpp:38-48), index order
+  void totals(double& effp, double& effr) const {
+    effp = 0;
+    effr = 0;
+    for (int32_t i = 0; i < h.n; ++i) {
+      const int32_t p = h.cls_pt_off[h.comp_class[i]] + ch[i];
+      effp += static_cast<double>(planned_energy(i)) -
+              h.watts * static_cast<double>(pt[i]) * static_cast<double>(h.quantum) * 1e-3;
+      effr += static_cast<double>(h.pt_energy[p]) -
+              h.watts * static_cast<double>(h.pt_time[p]) * static_cast<double>(h.quantum) * 1e-3;
+    }
+  }
+};
+
+pb_status check_index(const pb_batch* b, int32_t k, int32_t which) {
+  pb_frontier_summary s;
+  const pb_status st = pb_batch_summary(b, k, &s);
+  if (st != PB_OK) return st;
+  if (which < 0 || which > s.steps) return fail(PB_ERR_INVALID_ARGUMENT, "schedule index out of range");
+  return PB_OK;
+}
+
+// nlohmann::json's number layout for a double (shortest round-trip digits;
+// fixed notation for decimal exponents in (-4, 15], else d.ddde+XX; ".0" on
+// integral values), as serde.hpp's dump() writes round3 values.
+std::string json_double(double v) {
+  if (v == 0) return std::signbit(v) ? "-0.0" : "0.0";
+  char sci[64];
+  const auto r = std::to_chars(sci, sci + sizeof sci, v, std::chars_format::scientific);
+  std::string t(sci, r.ptr);
+  std::string out;
+  if (t[0] == '-') {
+    out = "-";
+    t = t.substr(1);
+  }
+  const size_t epos = t.find('e');
+  std::string digits = t.substr(0, epos);
+  const int e10 = std::stoi(t.substr(epos + 1));
+  digits.erase(std::remove(digits.begin(), digits.end(), '.'), digits.end());
+  const int len = static_cast<int>(digits.size());
+  const int n = e10 + 1;  // position of the decimal point
+  if (len <= n && n <= 15) {
+    out += digits + std::string(n - len, '0') + ".0";
+  } else if (0 < n && n <= 15) {
+    out += digits.substr(0, n) + "." + digits.substr(n);
+  } else if (-4 < n && n <= 0) {
+    out += "0." + std::string(-n, '0') + digits;
+  } else {
+    out += digits.substr(0, 1);
+    if (len > 1) out += "." + digits.substr(1);
+    const int e = n - 1;
+    char eb[16];
+    std::snprintf(eb, sizeof eb, "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
+    out += eb;
+  }
+  return out;
+}
+
+double round3(double v) { return std::round(v * 1000.0) / 1000.0; }  // serde.hpp:30
+
+pb_status emit(const std::string& text, char* buf, int64_t cap, int64_t* len) {
+  if (len) *len = static_cast<int64_t>(text.size());
+  if (buf) {
+    if (cap < static_cast<int64_t>(text.size())) return fail(PB_ERR_INVALID_ARGUMENT, "output buffer too small");
+    std::memcpy(buf, text.data(), text.size());
+  }
+  return PB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 pb_status pb_batch_schedule(const pb_batch* b, int32_t k, int32_t which, int64_t* planned_t,
                             int64_t* planned_e, int32_t* freq_mhz, int64_t* realized_t,
                             int64_t* realized_e, double* eff_planned, double* eff_realized) {
-  pb_frontier_summary s;
-  pb_status st = pb_batch_summary(b, k, &s);
+  const pb_status st = check_index(b, k, which);
   if (st != PB_OK) return st;
-  if (which < 0 || which > s.steps) return fail(PB_ERR_INVALID_ARGUMENT, "schedule index out of range");
-  const HostInst& h = b->insts[k];
-  const int32_t n = h.n;
-  std::vector<int64_t> pt(n);
-  std::vector<int32_t> ch(n);
-  auto choose = [&](int32_t c, int64_t t) {
-    int32_t chosen = 0;
-    for (int32_t p = h.cls_pt_off[c]; p < h.cls_pt_off[c + 1]; ++p)
-      if (h.pt_time[p] <= t) chosen = p - h.cls_pt_off[c];
-    return chosen;
-  };
-  for (int32_t i = 0; i < n; ++i) {
-    const int32_t c = h.comp_class[i];
-    pt[i] = !h.start.empty() ? h.start[i] : (h.cls_const[c] ? h.pt_time[h.cls_pt_off[c]] : h.cls_trange[2 * c + 1]);
-    ch[i] = choose(c, pt[i]);
-  }
-  const pb_point* pts = reinterpret_cast<const pb_point*>(b->out.data() + b->out_points[k]);
-  const int32_t* ids = b->pool_ids.data() + b->pool_base[k];
-  const uint8_t* cho = b->pool_choice.data() + b->pool_base[k];
-  for (int32_t q = 1; q <= which; ++q) {
-    const pb_point& p = pts[q];
-    const int32_t cnt = p.n_sped + p.n_slowed;
-    for (int32_t j = p.id_begin; j < p.id_begin + cnt; ++j) {
-      const int32_t x = ids[j];
-      const int32_t i = (x > 0 ? x : -x) - 1;
-      pt[i] += x > 0 ? -p.step_size : p.step_size;
-      ch[i] = cho[j];
-    }
-  }
-  double effp = 0, effr = 0;
-  for (int32_t i = 0; i < n; ++i) {
-    const int32_t c = h.comp_class[i];
-    const int32_t p = h.cls_pt_off[c] + ch[i];
-    int64_t e;
-    if (h.cls_const[c]) {
-      e = h.pt_energy[h.cls_pt_off[c]];
-    } else {
-      const int64_t lo = h.cls_trange[2 * c], hi = h.cls_trange[2 * c + 1];
-      const int64_t t = pt[i];
-      const double v = (t >= lo && t <= hi)
-                           ? b->tables[b->cls_tab[k][c] + (t - lo)]
-                           : h.cls_curve[3 * c] * std::exp(h.cls_curve[3 * c + 1] * static_cast<double>(t)) +
-                                 h.cls_curve[3 * c + 2];
-      e = static_cast<int64_t>(std::llround(v));
-    }
-    if (planned_t) planned_t[i] = pt[i];
-    if (planned_e) planned_e[i] = e;
+  Replay r(b, k);
+  r.advance_to(which);
+  const HostInst& h = r.h;
+  for (int32_t i = 0; i < h.n; ++i) {
+    const int32_t p = h.cls_pt_off[h.comp_class[i]] + r.ch[i];
+    if (planned_t) planned_t[i] = r.pt[i];
+    if (planned_e) planned_e[i] = r.planned_energy(i);
     if (freq_mhz) freq_mhz[i] = h.pt_freq[p];
     if (realized_t) realized_t[i] = h.pt_time[p];
     if (realized_e) realized_e[i] = h.pt_energy[p];
-    // effective_total (frontier.hpp:51-57; units.hpp:38-48), index order
-    effp += static_cast<double>(e) - h.watts * static_cast<double>(pt[i]) * static_cast<double>(h.quantum) * 1e-3;
-    effr += static_cast<double>(h.pt_energy[p]) -
-            h.watts * static_cast<double>(h.pt_time[p]) * static_cast<double>(h.quantum) * 1e-3;
   }
+  double effp, effr;
+  r.totals(effp, effr);
   if (eff_planned) *eff_planned = effp;
   if (eff_realized) *eff_realized = effr;
   return PB_OK;
+}
+
+pb_status pb_batch_frontier_csv(const pb_batch* b, int32_t k, int64_t quantum_us, char* buf, int64_t cap,
+                                int64_t* len) {
+  const pb_status st = check_index(b, k, 0);
+  if (st != PB_OK) return st;
+  pb_frontier_summary s;
+  pb_batch_summary(b, k, &s);
+  Replay r(b, k);
+  std::string out = "t_planned_us,t_realized_us,energy_planned_mj,energy_realized_mj,schedule_id\n";
+  char line[160];
+  for (int32_t q = 0; q <= s.steps; ++q) {
+    r.advance_to(q);
+    double effp, effr;
+    r.totals(effp, effr);
+    std::snprintf(line, sizeof line, "%lld,%lld,%.3f,%.3f,%d\n",
+                  static_cast<long long>(r.pts[q].t_planned * quantum_us),
+                  static_cast<long long>(r.pts[q].t_realized * quantum_us), effp, effr, q);
+    out += line;
+  }
+  return emit(out, buf, cap, len);
+}
+
+pb_status pb_batch_schedule_json(const pb_batch* b, int32_t k, int32_t which, int64_t quantum_us, char* buf,
+                                 int64_t cap, int64_t* len) {
+  const pb_status st = check_index(b, k, which);
+  if (st != PB_OK) return st;
+  Replay r(b, k);
+  r.advance_to(which);
+  double effp, effr;
+  r.totals(effp, effr);
+  const HostInst& h = r.h;
+  std::string o;
+  o.reserve(64 + 200 * static_cast<size_t>(h.n));
+  auto i64 = [](int64_t v) { return std::to_string(v); };
+  o += "{\n  \"schedule_id\": " + std::to_string(which) + ",\n";
+  o += "  \"t_planned_us\": " + i64(r.pts[which].t_planned * quantum_us) + ",\n";
+  o += "  \"eff_planned_mj\": " + json_double(round3(effp)) + ",\n";
+  o += "  \"t_realized_us\": " + i64(r.pts[which].t_realized * quantum_us) + ",\n";
+  o += "  \"eff_realized_mj\": " + json_double(round3(effr)) + ",\n";
+  o += "  \"computations\": [";
+  for (int32_t i = 0; i < h.n; ++i) {
+    const int32_t p = h.cls_pt_off[h.comp_class[i]] + r.ch[i];
+    o += i ? ",\n    {\n" : "\n    {\n";
+    o += "      \"id\": " + std::to_string(i) + ",\n";
+    o += "      \"freq_mhz\": " + std::to_string(h.pt_freq[p]) + ",\n";
+    o += "      \"t_planned_us\": " + i64(r.pt[i] * quantum_us) + ",\n";
+    o += "      \"e_planned_mj\": " + i64(r.planned_energy(i)) + ",\n";
+    o += "      \"t_realized_us\": " + i64(h.pt_time[p] * quantum_us) + ",\n";
+    o += "      \"e_realized_mj\": " + i64(h.pt_energy[p]) + "\n    }";
+  }
+  o += h.n ? "\n  ]\n}\n" : "]\n}\n";
+  return emit(o, buf, cap, len);
 }
 
 pb_status pb_batch_profile(const pb_batch* b, int64_t* out, int32_t n) {

@@ -143,6 +143,21 @@ class FrontierBatch:
                                          N.ptr(st, C.c_int32), buf))
         return np.ctypeslib.as_array(buf).copy().reshape(len(self), len(f))
 
+    def _text(self, fn, *args) -> str:
+        n = C.c_int64()
+        N.check(fn(self._h, *args, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        N.check(fn(self._h, *args, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value].decode()
+
+    def frontier_csv(self, k: int, quantum_us: int = 1) -> str:
+        """frontier.csv of instance k (serde.hpp frontier_csv)."""
+        return self._text(N.lib.pb_batch_frontier_csv, k, quantum_us)
+
+    def schedule_json(self, k: int, which: int, quantum_us: int = 1) -> str:
+        """schedules/schedule_<which>.json of instance k (serde.hpp write_frontier_artifacts)."""
+        return self._text(N.lib.pb_batch_schedule_json, k, which, quantum_us)
+
     # -- results
     def summary(self, k: int) -> N.FrontierSummary:
         s = N.FrontierSummary()

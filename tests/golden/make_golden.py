@@ -16,7 +16,9 @@ Fixtures (JSON lines, gzip):
   savings.jsonl.gz    straggler_savings rows (baselines.hpp:162-188) on the
                       reference frontier, 8 pipelines, the config-4 factor sweep
 
-    python tests/golden/make_golden.py [walks|flow|slack|savings ...]
+  artifacts.jsonl.gz  frontier.csv + schedule_<k>.json bytes (serde.hpp:194-257)
+
+    python tests/golden/make_golden.py [walks|flow|slack|savings|artifacts ...]
   batch_small.jsonl.gz  small config-5 style G9 instances (summaries only)
 """
 import gzip
@@ -49,7 +51,7 @@ SAVINGS_FACTORS = "1.0,1.05,1.1,1.2,1.3,1.5"  # SURVEY §8d config-4 straggler s
 def main():
     if not os.path.exists(DRIVER):
         sys.exit("build the reference driver first: make -C oracle ref")
-    parts = set(sys.argv[1:]) or {"walks", "flow", "slack", "savings"}
+    parts = set(sys.argv[1:]) or {"walks", "flow", "slack", "savings", "artifacts"}
     walk_specs = ["diamond", "lone:1000:9000:3000:5000", "lone:1000:9000:3000:5000:800",
                   "lone:1000:5000:11000:800", "config:1", "config:2"]
     walk_specs += [f"grid:{s}:{1 + s % 3}:{1 + s % 4}" for s in range(1, 41)]
@@ -67,6 +69,9 @@ def main():
         sav = [w for w in walk_specs if not w.startswith("cubic")]  # cubic walks stop early (infeasible)
         sav += [f"g9:4:{8 + s}:10:1.1:{s}:{s % 4}:{[1.0, 1.1, 1.3, 1.5][s % 4]}" for s in range(6)]
         write("savings.jsonl.gz", run("savings", "8", SAVINGS_FACTORS, *sav))
+    if "artifacts" in parts:
+        art = ["diamond", "lone:1000:9000:3000:5000", "config:1", "grid:3:1:4", "grid:101:4:3:4", "g9:3:5:9:1.2:7:1:1.5"]
+        write("artifacts.jsonl.gz", run("artifacts", "1", *art) + run("artifacts", "10", "config:1", "diamond"))
 
 
 if __name__ == "__main__":

@@ -306,3 +306,43 @@ def test_straggler_sweep_matches_reference(walks):
             scale = (P - 1) * abs(got["all_max_mj"])
             assert abs(got["savings_mj"] - ref["savings_mj"]) <= 1e-9 * scale, (r["spec"], ref, got)
             assert abs(got["savings_pct"] - ref["savings_pct"]) <= 1e-9 * 100, (r["spec"], ref, got)
+
+
+def test_artifacts_byte_identical_to_reference_writer(walks):
+    """frontier.csv and schedules/schedule_<k>.json expanded from the delta log
+    (pb_batch_frontier_csv / pb_batch_schedule_json) against the bytes the
+    reference writer produces (serde.hpp:194-257, 304-316), quantum 1 and 10."""
+    from conftest import load_golden
+    recs = load_golden("artifacts.jsonl.gz")
+    b = pb.FrontierBatch()
+    for r in recs:
+        spec = r["spec"]
+        if spec in walks:
+            dag, model, tau = instance_from_golden(walks[spec])
+            b.add(dag, model, tau)
+        else:
+            _, N_, M_, B_, imb, seed, st, phi = spec.split(":")
+            b.add_g9(g9.G9Params(int(N_), int(M_), int(B_), float(imb), int(seed), int(st), float(phi)))
+    b.run(0)
+    for k, r in enumerate(recs):
+        assert b.frontier_csv(k, r["quantum"]) == r["csv"], r["spec"]
+        for which, text in r["schedules"].items():
+            assert b.schedule_json(k, int(which), r["quantum"]) == text, (r["spec"], which)
+
+
+def test_lone_artifacts_match_test_serde_cpp():
+    """test_serde.cpp:252-259 golden CSV of the lone walk."""
+    dag, model = _lone(1000, 9000, 3000, 5000)
+    b = pb.FrontierBatch()
+    b.add(dag, model, 1000)
+    b.run(0)
+    assert b.frontier_csv(0) == ("t_planned_us,t_realized_us,energy_planned_mj,energy_realized_mj,schedule_id\n"
+                                 "3000,3000,4775.000,4775.000,0\n"
+                                 "2000,1000,6558.000,8925.000,1\n"
+                                 "1000,1000,8925.000,8925.000,2\n")
+    assert "30000,30000,4775.000" in b.frontier_csv(0, 10)
+    assert b.schedule_json(0, 1).replace("\n", "").replace(" ", "") == (
+        '{"schedule_id":1,"t_planned_us":2000,"eff_planned_mj":6558.0,'
+        '"t_realized_us":1000,"eff_realized_mj":8925.0,'
+        '"computations":[{"id":0,"freq_mhz":1400,"t_planned_us":2000,"e_planned_mj":6708,'
+        '"t_realized_us":1000,"e_realized_mj":9000}]}')
