@@ -260,6 +260,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         b.launch()
     D.barrier()
+    launches0 = b.stats().kernel_launches
     kernel_ms = []
     with ClockSampler(device) as clk:
         for _ in range(args.steps):
@@ -267,6 +268,7 @@ def run_ours(args):
             kernel_ms.append(b.launch())  # synchronizes its stream on both sides
             D.barrier()
     st = b.stats()
+    timed_launches = st.kernel_launches - launches0  # walker + cooperative kernels per step
     b.fetch()
     points = steps = 0
     bad = 0
@@ -315,7 +317,7 @@ def run_ours(args):
         "iterations_per_s": total_steps * args.steps / t_dev,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(st_e2e.h2d_bytes),
                 "d2h_bytes_per_step": int(st_e2e.d2h_bytes)},
-        "gpu_launches": args.steps,
+        "gpu_launches": int(timed_launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None,
                      "traffic": traffic.get("bytes_per_launch") if traffic else None,

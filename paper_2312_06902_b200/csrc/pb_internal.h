@@ -75,7 +75,8 @@ void build_net(int32_t V, const std::vector<int32_t>& tail, const std::vector<in
 // caller's id; node-DAG virtual source n, sink n+1.  Edge-centric network
 // (dag.hpp:209-224): computation i -> nodes 2i (start), 2i+1 (end), source
 // 2n, sink 2n+1; edge i = computation edge 2i -> 2i+1, edge n+j = dependency
-// j (caller's order), edge n+ne = phase-A return arc sink -> source
+// j (network order, sorted by head then tail; dep_orig maps back to the
+// caller's edge index), edge n+ne = phase-A return arc sink -> source
 // (flow.hpp:196-200).
 struct DevInst {
   int32_t n, ne, n_levels, mode;
@@ -95,7 +96,8 @@ struct DevInst {
   const int32_t* pin;
   const int32_t* pout_off;    // [n + 1] computation successors
   const int32_t* pout;
-  const int2* dep_nd;         // [ne] node-DAG endpoints (n = source, n + 1 = sink)
+  const int2* dep_nd;         // [ne] node-DAG endpoints (n = source, n + 1 = sink), network order
+  const int32_t* dep_orig;    // [ne] network dependency index -> caller's edge index
   // edge-centric flow network
   const int32_t* inc_off;     // [V + 1]
   const IEnt* ient;           // [2E]

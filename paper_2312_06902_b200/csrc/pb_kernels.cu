@@ -1656,7 +1656,7 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
         he = W.fin[uv.y].x - W.durp[uv.y];
         hl = ms - W.tl[uv.y].x;
       }
-      O.critical[n + j] = te == tl && he == hl && te == he;
+      O.critical[n + I.dep_orig[j]] = te == tl && he == hl && te == he;
     }
     __syncwarp();
   }
