@@ -351,6 +351,9 @@ struct DeviceRun {
   size_t out_bytes = 0;
   int32_t slots = 0;
   pb::WsLayout ws{};
+  // allocated capacities (buffers are reused across runs while they fit)
+  size_t cap_static = 0, cap_out = 0, cap_ws = 0, cap_insts = 0, cap_order = 0;
+  long long cap_pool = 0;
   cudaStream_t stream = nullptr, stream_big = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_big = nullptr;
   WidePlan wide;
@@ -388,7 +391,8 @@ struct pb_batch {
   // outputs (host copies)
   std::vector<size_t> out_points, out_summary;
   std::vector<int32_t> cap_points;
-  std::vector<char> out;  // host results: points + summaries
+  std::vector<char> out;  // host results of a multi-device run (stitched)
+  const char* outp = nullptr;  // host results: R.h_out (pinned) or out.data()
   std::vector<int32_t> pool_ids;  // delta pool (used prefix)
   std::vector<uint8_t> pool_choice;
   std::vector<long long> pool_base;  // per instance: offset of its id_begin values
@@ -397,7 +401,12 @@ struct pb_batch {
   DeviceRun run;
   pb_run_stats stats{};
   int64_t prof[pb::kPrSlots] = {};
-  ~pb_batch() { run.release(); }
+  char* h_static = nullptr;  // pinned staging of the packed static blob (reused)
+  size_t h_static_cap = 0;
+  ~pb_batch() {
+    run.release();
+    if (h_static) cudaFreeHost(h_static);
+  }
 };
 
 namespace {
@@ -406,7 +415,7 @@ namespace {
 // offsets (converted to device pointers once the blob is uploaded).
 struct Packed {
   long long pool_cap = 0;
-  Blob stat;
+  size_t stat_bytes = 0;  // packed static blob (tables first), in pb_batch::h_static
   std::vector<pb::DevInst> dev;
   std::vector<std::array<size_t, 32>> offs;
   size_t out_bytes = 0;
@@ -448,6 +457,57 @@ void fill_shape(pb::DevInst& d, const HostInst& h) {
   d.ret_ph = h.net.epos[d.E - 1].y;
 }
 
+// Every static section of instance k in blob order: f(slot, data, bytes).
+// With fill = false only the sizes are needed (data may be null).
+template <class F>
+void instance_sections(const pb_batch* b, size_t k, bool fill, F&& f) {
+  const HostInst& h = b->insts[k];
+  auto vec = [&](int slot, const auto& v) { f(slot, static_cast<const void*>(v.data()), v.size() * sizeof(v[0])); };
+  vec(O_ORIG, h.orig);
+  vec(O_CLASS, h.icls);
+  vec(O_CFLAG, h.cflag);
+  vec(O_LVLOFF, h.lvl_off);
+  vec(O_FROW, h.frow);
+  vec(O_BROW, h.brow);
+  vec(O_PINOFF, h.pin_off);
+  vec(O_PIN, h.pin);
+  vec(O_POUTOFF, h.pout_off);
+  vec(O_POUT, h.pout);
+  vec(O_DEPND, h.dep_nd);
+  vec(O_INCOFF, h.net.inc_off);
+  vec(O_IENT, h.net.ient);
+  vec(O_EPOS, h.net.epos);
+  vec(O_DEPORIG, h.dep_orig);
+  vec(O_CCONST, h.cls_const);
+  const size_t nc = h.cls_const.size();
+  std::vector<int64_t> tmin, tmax;
+  std::vector<pb::CompRec> rec;
+  if (fill) {
+    tmin.resize(nc);
+    tmax.resize(nc);
+    for (size_t c = 0; c < nc; ++c) {
+      tmin[c] = h.cls_trange[2 * c];
+      tmax[c] = h.cls_trange[2 * c + 1];
+    }
+    rec.resize(h.n);
+    for (int32_t i = 0; i < h.n; ++i) {
+      const int32_t c = h.icls[i];
+      const bool cst = h.cls_const[c] != 0;
+      rec[i] = pb::CompRec{cst ? 0 : h.cls_trange[2 * c], cst ? 0 : h.cls_trange[2 * c + 1],
+                           cst ? -1 : b->cls_tab[k][c], h.net.epos[i].x, h.net.epos[i].y};
+    }
+  }
+  f(O_CTMIN, tmin.data(), sizeof(int64_t) * nc);
+  f(O_CTMAX, tmax.data(), sizeof(int64_t) * nc);
+  vec(O_CTAB, b->cls_tab[k]);
+  vec(O_CPOFF, h.cls_pt_off);
+  vec(O_PTIME, h.pt_time);
+  vec(O_PENERGY, h.pt_energy);
+  if (!h.istart.empty()) vec(O_START, h.istart);
+  vec(O_CURVE, h.cls_curve);
+  f(O_CREC, rec.data(), sizeof(pb::CompRec) * static_cast<size_t>(h.n));
+}
+
 void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_scale) {
   const size_t N = b->insts.size();
   // curve tables, deduplicated by (a, b, c, t_min, t_max) bit patterns
@@ -477,7 +537,6 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
       b->cls_tab[k][c] = it->second;
     }
   }
-  const size_t tables_off = P.stat.put(b->tables);
   P.dev.assign(N, pb::DevInst{});
   P.offs.assign(N, {});
   cap_points.assign(N, 0);
@@ -488,34 +547,42 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
     out = at + bytes;
     return at;
   };
+  // layout pass: section offsets of every instance (tables at offset 0)
+  size_t off = b->tables.size() * sizeof(double);
+  for (size_t k = 0; k < N; ++k) {
+    auto& o = P.offs[k];
+    o[O_START] = SIZE_MAX;
+    instance_sections(b, k, false, [&](int slot, const void*, size_t bytes) {
+      off = (off + 255) / 256 * 256;
+      o[slot] = off;
+      off += bytes;
+    });
+  }
+  P.stat_bytes = std::max<size_t>(off, 256);
+  if (b->h_static_cap < P.stat_bytes) {
+    if (b->h_static) cudaFreeHost(b->h_static);
+    b->h_static = nullptr;
+    b->h_static_cap = 0;
+    ck(cudaMallocHost(&b->h_static, P.stat_bytes + P.stat_bytes / 4), "malloc pinned static");
+    b->h_static_cap = P.stat_bytes + P.stat_bytes / 4;
+  }
+  std::memcpy(b->h_static, b->tables.data(), b->tables.size() * sizeof(double));
+  // fill pass: instances copied in parallel straight into pinned memory
+  {
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16u));
+    std::vector<std::thread> pool_t;
+    for (unsigned t = 0; t < nt; ++t)
+      pool_t.emplace_back([&, t] {
+        for (size_t k = t; k < N; k += nt)
+          instance_sections(b, k, true, [&](int slot, const void* p, size_t bytes) {
+            if (bytes) std::memcpy(b->h_static + P.offs[k][slot], p, bytes);
+          });
+      });
+    for (auto& th : pool_t) th.join();
+  }
   for (size_t k = 0; k < N; ++k) {
     const HostInst& h = b->insts[k];
     auto& o = P.offs[k];
-    std::vector<int64_t> tmin(h.cls_const.size()), tmax(h.cls_const.size());
-    for (size_t c = 0; c < h.cls_const.size(); ++c) {
-      tmin[c] = h.cls_trange[2 * c];
-      tmax[c] = h.cls_trange[2 * c + 1];
-    }
-    put_static(P.stat, h, o);
-    o[O_CCONST] = P.stat.put(h.cls_const);
-    o[O_CTMIN] = P.stat.put(tmin);
-    o[O_CTMAX] = P.stat.put(tmax);
-    o[O_CTAB] = P.stat.put(b->cls_tab[k]);
-    o[O_CPOFF] = P.stat.put(h.cls_pt_off);
-    o[O_PTIME] = P.stat.put(h.pt_time);
-    o[O_PENERGY] = P.stat.put(h.pt_energy);
-    o[O_START] = h.istart.empty() ? SIZE_MAX : P.stat.put(h.istart);
-    o[O_CURVE] = P.stat.put(h.cls_curve);
-    {
-      std::vector<pb::CompRec> rec(h.n);
-      for (int32_t i = 0; i < h.n; ++i) {
-        const int32_t c = h.icls[i];
-        const bool cst = h.cls_const[c] != 0;
-        rec[i] = pb::CompRec{cst ? 0 : h.cls_trange[2 * c], cst ? 0 : h.cls_trange[2 * c + 1],
-                             cst ? -1 : b->cls_tab[k][c], h.net.epos[i].x, h.net.epos[i].y};
-      }
-      o[O_CREC] = P.stat.put(rec);
-    }
     const int64_t est = static_cast<int64_t>(static_cast<double>(h.est_steps) * cap_scale);
     cap_points[k] = static_cast<int32_t>(std::min<int64_t>(est + 8, INT32_MAX / 2));
     pool += est * 12 + 2 * int64_t{h.n} + 64;
@@ -535,7 +602,6 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
   }
   P.out_bytes = out;
   P.pool_cap = std::min<long long>(pool, (1ll << 31) - 1);
-  (void)tables_off;
   // LPT: largest estimated work first
   P.order.resize(N);
   std::iota(P.order.begin(), P.order.end(), 0);
@@ -613,9 +679,10 @@ WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int s
   int n = env_int("PB_WIDE", -1);
   if (n < 0) {
     n = 0;
-    // measured on the 4096 batch: the top ~50 walks (>= 88% of the largest
-    // estimated work) on 2-warp CTAs shorten the critical walk by ~6%
-    const int permille = env_int("PB_WIDE_PERMILLE", 880);
+    // opt-in (PB_WIDE_PERMILLE=880 measured ~6% on the 4096 batch: the top
+    // ~50 walks on 2-warp CTAs).  Off by default: two runs hung
+    // intermittently with it on and the cause is not found yet.
+    const int permille = env_int("PB_WIDE_PERMILLE", 0);
     if (permille > 0 && N > int64_t{sms} * per_sm) {
       const double top = static_cast<double>(b->insts[order[0]].work);
       while (n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;
@@ -638,30 +705,59 @@ int32_t device_slots(int device, int64_t n_walk, const pb::WsLayout& ws, const W
       std::max<int64_t>(std::min<int64_t>(n_walk, int64_t{sms} * per_sm - wide_warps), std::min<int64_t>(n_walk, 4)));
 }
 
+// (Re)allocates a device buffer only when the current one is too small.
+template <class T>
+void ensure_device(T*& ptr, size_t& cap, size_t bytes, const char* what) {
+  bytes = std::max<size_t>(bytes, 256);
+  if (ptr && cap >= bytes) return;
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+  ck(cudaMalloc(reinterpret_cast<void**>(&ptr), bytes), what);
+  cap = bytes;
+}
+
+// Packs the batch (host, parallel, into pinned staging) and uploads it.
+// Device buffers, pinned buffers, streams and events persist across runs on
+// the same device and are only grown.
 pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
-  b->run.release();
+  DeviceRun& R = b->run;
+  if (R.device >= 0 && R.device != device) R.release();
   b->have_results = false;
   const size_t N = b->insts.size();
   if (N == 0) return PB_OK;
-  DeviceRun& R = b->run;
   ck(cudaSetDevice(device), "cudaSetDevice");
-  R.device = device;
+  if (R.device < 0) {
+    R.device = device;
+    ck(cudaStreamCreateWithFlags(&R.stream, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&R.stream_big, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&R.ev_big, cudaEventDisableTiming), "event");
+    ck(cudaEventCreate(&R.ev0), "event");
+    ck(cudaEventCreate(&R.ev1), "event");
+    ck(cudaMalloc(&R.d_counter, 2 * sizeof(int32_t)), "malloc counter");
+    ck(cudaMalloc(&R.d_counters, sizeof(pb::RunCounters)), "malloc counters");
+    ck(cudaMalloc(&R.d_pool_cursor, sizeof(unsigned long long)), "malloc cursor");
+  }
   Packed P;
   std::vector<int32_t> capp;
   pack(b, P, capp, cap_scale);
   const size_t tables_off = 0;  // tables are the first section of the blob
-  ck(cudaStreamCreateWithFlags(&R.stream, cudaStreamNonBlocking), "stream");
-  ck(cudaStreamCreateWithFlags(&R.stream_big, cudaStreamNonBlocking), "stream");
-  ck(cudaEventCreateWithFlags(&R.ev_big, cudaEventDisableTiming), "event");
-  ck(cudaEventCreate(&R.ev0), "event");
-  ck(cudaEventCreate(&R.ev1), "event");
   cudaEvent_t h0, h1;
   ck(cudaEventCreate(&h0), "event");
   ck(cudaEventCreate(&h1), "event");
-  ck(cudaMalloc(&R.d_static, std::max<size_t>(P.stat.bytes.size(), 256)), "malloc static");
+  ensure_device(R.d_static, R.cap_static, P.stat_bytes, "malloc static");
   R.out_bytes = std::max<size_t>(P.out_bytes, 256);
-  ck(cudaMalloc(&R.d_out, R.out_bytes), "malloc out");
-  ck(cudaMallocHost(&R.h_out, R.out_bytes), "malloc pinned out");
+  if (R.cap_out < R.out_bytes) {
+    if (R.d_out) cudaFree(R.d_out);
+    if (R.h_out) cudaFreeHost(R.h_out);
+    R.d_out = nullptr;
+    R.h_out = nullptr;
+    R.cap_out = 0;
+    const size_t want = R.out_bytes + R.out_bytes / 4;
+    ck(cudaMalloc(&R.d_out, want), "malloc out");
+    ck(cudaMallocHost(&R.h_out, want), "malloc pinned out");
+    R.cap_out = want;
+  }
   bind_device(P, R.d_static, R.d_out, tables_off);
   R.ws = pb::make_ws_layout(P.max_n, P.max_v, P.max_e);
   {
@@ -670,24 +766,26 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
     R.wide = choose_wide(b, P.order, sms, std::max(1, pb::walk_slots_per_sm(R.ws)));
   }
   R.slots = device_slots(device, static_cast<int64_t>(N) - R.wide.n, R.ws, R.wide);
-  ck(cudaMalloc(&R.d_ws, static_cast<size_t>(R.ws.stride) * (R.slots + R.wide.ctas)), "malloc workspace");
-  ck(cudaMalloc(&R.d_insts, sizeof(pb::DevInst) * N), "malloc insts");
-  ck(cudaMalloc(&R.d_order, sizeof(int32_t) * N), "malloc order");
-  ck(cudaMalloc(&R.d_counter, 2 * sizeof(int32_t)), "malloc counter");
-  ck(cudaMalloc(&R.d_counters, sizeof(pb::RunCounters)), "malloc counters");
+  ensure_device(R.d_ws, R.cap_ws, static_cast<size_t>(R.ws.stride) * (R.slots + R.wide.ctas), "malloc workspace");
+  ensure_device(R.d_insts, R.cap_insts, sizeof(pb::DevInst) * N, "malloc insts");
+  ensure_device(R.d_order, R.cap_order, sizeof(int32_t) * N, "malloc order");
   R.pool_cap = P.pool_cap;
-  ck(cudaMalloc(&R.d_pool_ids, sizeof(int32_t) * std::max<long long>(R.pool_cap, 1)), "malloc pool");
-  ck(cudaMalloc(&R.d_pool_choice, std::max<long long>(R.pool_cap, 1)), "malloc pool");
-  ck(cudaMalloc(&R.d_pool_cursor, sizeof(unsigned long long)), "malloc cursor");
+  if (R.cap_pool < std::max<long long>(R.pool_cap, 1)) {
+    if (R.d_pool_ids) cudaFree(R.d_pool_ids);
+    if (R.d_pool_choice) cudaFree(R.d_pool_choice);
+    R.d_pool_ids = nullptr;
+    R.d_pool_choice = nullptr;
+    R.cap_pool = 0;
+    const long long want = std::max<long long>(R.pool_cap, 1);
+    ck(cudaMalloc(&R.d_pool_ids, sizeof(int32_t) * want), "malloc pool");
+    ck(cudaMalloc(&R.d_pool_choice, want), "malloc pool");
+    R.cap_pool = want;
+  }
   ck(cudaEventRecord(h0, R.stream), "record");
-  ck(cudaMemcpyAsync(R.d_static, P.stat.bytes.data(), P.stat.bytes.size(), cudaMemcpyHostToDevice,
-                     R.stream),
-     "H2D static");
-  ck(cudaMemcpyAsync(R.d_insts, P.dev.data(), sizeof(pb::DevInst) * N, cudaMemcpyHostToDevice,
-                     R.stream),
+  ck(cudaMemcpyAsync(R.d_static, b->h_static, P.stat_bytes, cudaMemcpyHostToDevice, R.stream), "H2D static");
+  ck(cudaMemcpyAsync(R.d_insts, P.dev.data(), sizeof(pb::DevInst) * N, cudaMemcpyHostToDevice, R.stream),
      "H2D insts");
-  ck(cudaMemcpyAsync(R.d_order, P.order.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice,
-                     R.stream),
+  ck(cudaMemcpyAsync(R.d_order, P.order.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, R.stream),
      "H2D order");
   ck(cudaEventRecord(h1, R.stream), "record");
   ck(cudaStreamSynchronize(R.stream), "sync");
@@ -697,8 +795,7 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   cudaEventDestroy(h1);
   b->stats = pb_run_stats{};
   b->stats.h2d_ms = ms;
-  b->stats.h2d_bytes = static_cast<int64_t>(P.stat.bytes.size() + sizeof(pb::DevInst) * N +
-                                            sizeof(int32_t) * N);
+  b->stats.h2d_bytes = static_cast<int64_t>(P.stat_bytes + sizeof(pb::DevInst) * N + sizeof(int32_t) * N);
   return PB_OK;
 }
 
@@ -771,7 +868,7 @@ pb_status fetch_impl(pb_batch* b) {
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  b->out.assign(R.h_out, R.h_out + R.out_bytes);
+  b->outp = R.h_out;  // results stay in the pinned buffer until the next run
   b->stats.d2h_ms = ms;
   b->stats.d2h_bytes = static_cast<int64_t>(R.out_bytes + 5 * nused + sizeof used);
   b->have_results = true;
@@ -779,7 +876,7 @@ pb_status fetch_impl(pb_batch* b) {
 }
 
 const pb_frontier_summary& summary_of(const pb_batch* b, int32_t k) {
-  return *reinterpret_cast<const pb_frontier_summary*>(b->out.data() + b->out_summary[k]);
+  return *reinterpret_cast<const pb_frontier_summary*>(b->outp + b->out_summary[k]);
 }
 
 bool any_log_full(const pb_batch* b) {
@@ -1038,6 +1135,7 @@ pb_status pb_batch_run_multi(pb_batch* b, int32_t n_devices, const int32_t* devi
       b->stats.kernel_launches += s.stats.kernel_launches;
     }
     b->out = std::move(out);
+    b->outp = b->out.data();
     b->have_results = true;
     return PB_OK;
   });
@@ -1057,7 +1155,7 @@ pb_status pb_batch_points(const pb_batch* b, int32_t k, pb_point* out, int32_t c
   if (st != PB_OK) return st;
   const int32_t np = s.steps + 1;
   if (capacity < np) return fail(PB_ERR_INVALID_ARGUMENT, "points buffer too small");
-  std::memcpy(out, b->out.data() + b->out_points[k], sizeof(pb_point) * np);
+  std::memcpy(out, b->outp + b->out_points[k], sizeof(pb_point) * np);
   // id_begin: pool offsets on the device -> offsets into pb_batch_deltas()
   int32_t acc = 0;
   for (int32_t q = 1; q < np; ++q) {
@@ -1073,7 +1171,7 @@ pb_status pb_batch_deltas(const pb_batch* b, int32_t k, int32_t* ids, uint8_t* c
   pb_status st = pb_batch_summary(b, k, &s);
   if (st != PB_OK) return st;
   if (capacity < s.n_ids) return fail(PB_ERR_INVALID_ARGUMENT, "delta buffer too small");
-  const pb_point* pts = reinterpret_cast<const pb_point*>(b->out.data() + b->out_points[k]);
+  const pb_point* pts = reinterpret_cast<const pb_point*>(b->outp + b->out_points[k]);
   int32_t j = 0;
   for (int32_t q = 1; q <= s.steps; ++q) {
     const long long at = b->pool_base[k] + pts[q].id_begin;
@@ -1105,7 +1203,7 @@ struct Replay {
 
   Replay(const pb_batch* bb, int32_t kk)
       : b(bb), k(kk), h(bb->insts[kk]),
-        pts(reinterpret_cast<const pb_point*>(bb->out.data() + bb->out_points[kk])),
+        pts(reinterpret_cast<const pb_point*>(bb->outp + bb->out_points[kk])),
         ids(bb->pool_ids.data() + bb->pool_base[kk]), cho(bb->pool_choice.data() + bb->pool_base[kk]) {
     const int32_t n = h.n;
     pt.resize(n);

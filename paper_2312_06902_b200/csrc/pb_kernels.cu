@@ -48,6 +48,10 @@ constexpr int kBlock = 32 * kWarpsPerBlock;
 #define PB_MIN_BLOCKS 3
 #endif
 constexpr int kMinBlocks = PB_MIN_BLOCKS;  // walker blocks per SM the register budget must allow
+#ifndef PB_LANE_GROUP_LOG2
+#define PB_LANE_GROUP_LOG2 -1
+#endif
+constexpr int kLaneGroupLog2 = PB_LANE_GROUP_LOG2;  // >= 0 forces lanes per frontier node (experiments)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr long long kHuge = LLONG_MAX / 4;  // return-arc capacity (never binding)
 constexpr int kMaxEnds = 32;               // phase-B path ends kept per BFS
@@ -287,7 +291,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi) {
   const uint32_t snk_word = N.s_bits + 4u * (N.snk >> 5), snk_mask = 1u << (N.snk & 31);
   while (cnt > 0) {
     const int per = kCoop ? (cnt + nw - 1) / nw : cnt;
-    const int lg2 = per <= 8 ? 2 : (per <= 16 ? 1 : 0);
+    const int lg2 = kLaneGroupLog2 >= 0 ? kLaneGroupLog2 : (per <= 8 ? 2 : (per <= 16 ? 1 : 0));
     const int g = 1 << lg2;
     const int sub = ln & (g - 1);
     const int nxt = cur ^ 1;
