@@ -53,7 +53,14 @@ class Dist:
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            if backend == "nccl":
+            ndev = torch.cuda.device_count() if backend == "nccl" else 0
+            if backend == "nccl" and self.world > ndev:
+                # more ranks than GPUs (a 1-GPU smoke test of the N > 1 path):
+                # ranks share devices round-robin and NCCL cannot run two
+                # ranks on one device, so the plumbing falls back to gloo
+                backend = "gloo"
+            if ndev:
+                self.local = self.local % ndev
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend=backend)
             self.dist, self.torch = dist, torch
