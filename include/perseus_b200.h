@@ -35,8 +35,10 @@ typedef enum {
   PB_ERR_LOGIC = 3,            /* std::logic_error (flow.hpp:265; frontier.hpp:213) */
   PB_ERR_DOMAIN = 4,           /* DegenerateFit, std::domain_error (costmodel.hpp:50-52) */
   PB_ERR_CUDA = 5,             /* device failure (no reference counterpart) */
-  PB_ERR_UNSUPPORTED = 6       /* input outside what the device layout supports
+  PB_ERR_UNSUPPORTED = 6,      /* input outside what the device layout supports
                                   (e.g. a curve interval too long to tabulate) */
+  PB_ERR_BUDGET = 7            /* BudgetExceeded (oracle.hpp:17-19): assignment
+                                  space above the enumeration budget */
 } pb_status;
 
 /* Why a frontier walk ended (frontier.hpp:178-187). */
@@ -219,6 +221,24 @@ typedef struct {
  * NodeDag::num_stages of instance k. */
 pb_status pb_batch_straggler(pb_batch* b, int32_t n_factors, const double* factors, int32_t pipelines,
                              const int32_t* num_stages, pb_savings_row* out);
+
+/* ---- exhaustive oracle on the GPU -------------------- */
+/* brute_force_frontier (oracle.hpp:47-114) for instance `index`: every
+ * assignment of per-computation Pareto points enumerated on the device (one
+ * thread per assignment code; longest path + effective energy summed in
+ * index order exactly as simulate / detail::effective_total), the cheapest
+ * (first-enumerated on ties) per distinct iteration time kept, then the
+ * ascending-time, strictly-decreasing-energy frontier.  code = the
+ * reference's mixed-radix assignment code (last computation fastest).
+ * freq_mhz (optional) receives capacity x n frequencies, caller order. */
+typedef struct {
+  int64_t time;
+  double eff_energy_mj;
+  int64_t code;
+} pb_exact_point;
+pb_status pb_batch_brute_force(pb_batch* b, int32_t index, double combination_budget, int32_t device,
+                               pb_exact_point* points, int32_t* freq_mhz, int32_t capacity,
+                               int32_t* count);
 
 /* ---- component kernels, exposed for parity tests ----------------------- */
 /* annotate_slack (dag.hpp:233-286) for a batch of DAGs on one device.

@@ -19,6 +19,7 @@
 //                            frontier.csv + schedule_<k>.json bytes
 //                            (serde.hpp frontier_csv / schedule_json dump(2))
 //                            for the first, middle and last schedules
+//   brute <spec>...          brute_force_frontier (oracle.hpp:47-114) points
 //   savings <P> <factors,...> <spec>...
 //                            straggler_savings (baselines.hpp:162-188) on the
 //                            reference frontier: rows + the looked-up point
@@ -556,6 +557,28 @@ int mode_artifacts(int argc, char** argv) {
   return 0;
 }
 
+int mode_brute(int argc, char** argv) {
+  for (int i = 2; i < argc; ++i) {
+    const Instance in = make_instance(argv[i]);
+    nlohmann::ordered_json j;
+    j["spec"] = argv[i];
+    try {
+      const ExactFrontier ex = brute_force_frontier(in.dag, in.model);
+      nlohmann::ordered_json pts = nlohmann::ordered_json::array();
+      for (const auto& p : ex.points) {
+        std::uint64_t bitsv;
+        std::memcpy(&bitsv, &p.eff_energy_mj, 8);
+        pts.push_back({{"time", p.time}, {"eff_bits", std::to_string(bitsv)}, {"freq_mhz", p.freq_mhz}});
+      }
+      j["points"] = pts;
+    } catch (const BudgetExceeded&) {
+      j["budget_exceeded"] = true;
+    }
+    std::printf("%s\n", j.dump().c_str());
+  }
+  return 0;
+}
+
 int mode_budget(int argc, char** argv) {
   const double budget = std::stod(argv[2]);
   const int threads = std::max(1, std::stoi(argv[3]));
@@ -630,6 +653,7 @@ int main(int argc, char** argv) {
     if (mode == "budget") return mode_budget(argc, argv);
     if (mode == "savings") return mode_savings(argc, argv);
     if (mode == "artifacts") return mode_artifacts(argc, argv);
+    if (mode == "brute") return mode_brute(argc, argv);
     if (mode == "fit") {
       for (int i = 2; i < argc; ++i) {
         const Instance in = make_instance(argv[i]);

@@ -21,6 +21,7 @@ PB_ERR_LOGIC = 3
 PB_ERR_DOMAIN = 4
 PB_ERR_CUDA = 5
 PB_ERR_UNSUPPORTED = 6
+PB_ERR_BUDGET = 7
 
 STOP_AT_TMIN = 0
 STOP_INFEASIBLE = 1
@@ -46,6 +47,10 @@ class UnsupportedInput(NotImplementedError):
     """Documented divergence: a curve evaluated outside its profiled interval."""
 
 
+class BudgetExceeded(RuntimeError):
+    """perseus::BudgetExceeded (oracle.hpp:17-19)."""
+
+
 _EXC = {
     PB_ERR_INVALID_ARGUMENT: ValueError,
     PB_ERR_OVERFLOW: OverflowError,
@@ -53,6 +58,7 @@ _EXC = {
     PB_ERR_DOMAIN: DegenerateFit,
     PB_ERR_CUDA: CudaError,
     PB_ERR_UNSUPPORTED: UnsupportedInput,
+    PB_ERR_BUDGET: BudgetExceeded,
 }
 
 i32p = C.POINTER(C.c_int32)
@@ -142,6 +148,10 @@ class SavingsRow(C.Structure):
     ]
 
 
+class ExactPoint(C.Structure):
+    _fields_ = [("time", C.c_int64), ("eff_energy_mj", C.c_double), ("code", C.c_int64)]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -170,6 +180,8 @@ def _load() -> C.CDLL:
         "pb_batch_profile": (C.c_int, [P, i64p, C.c_int32]),
         "pb_batch_straggler": (C.c_int, [P, C.c_int32, f64p, C.c_int32, i32p, C.POINTER(SavingsRow)]),
         "pb_batch_frontier_csv": (C.c_int, [P, C.c_int32, C.c_int64, C.c_char_p, C.c_int64, i64p]),
+        "pb_batch_brute_force": (C.c_int, [P, C.c_int32, C.c_double, C.c_int32, C.POINTER(ExactPoint), i32p,
+                                           C.c_int32, i32p]),
         "pb_batch_schedule_json": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, C.c_char_p, C.c_int64, i64p]),
         "pb_batch_destroy": (None, [P]),
         "pb_annotate_slack_batch": (C.c_int, [C.c_int32, C.c_int32, i32p, i32p, i32p, i32p, i64p,
@@ -199,7 +211,7 @@ EXPORTED = (
     "pb_batch_run_multi", "pb_batch_summary", "pb_batch_points", "pb_batch_deltas", "pb_batch_schedule",
     "pb_batch_stats", "pb_batch_profile", "pb_batch_destroy", "pb_annotate_slack_batch", "pb_flow_min_cut_batch",
     "pb_g9_stage_bases", "pb_g9_batch_params", "pb_g9_profile", "pb_batch_add_g9", "pb_batch_straggler",
-    "pb_batch_frontier_csv", "pb_batch_schedule_json",
+    "pb_batch_frontier_csv", "pb_batch_schedule_json", "pb_batch_brute_force",
 )
 
 

@@ -1453,6 +1453,115 @@ pb_status pb_batch_straggler(pb_batch* b, int32_t n_factors, const double* facto
   });
 }
 
+// ------------------------------------------------------- exhaustive oracle
+
+pb_status pb_batch_brute_force(pb_batch* b, int32_t k, double budget, int32_t device, pb_exact_point* points,
+                               int32_t* freq_mhz, int32_t capacity, int32_t* count) {
+  if (!b || !count || k < 0 || k >= static_cast<int32_t>(b->insts.size()))
+    return fail(PB_ERR_INVALID_ARGUMENT, "bad instance index");
+  const HostInst& h = b->insts[k];
+  const int32_t n = h.n;
+  // mixed radix over caller ids, last computation fastest (oracle.hpp:53-66)
+  double combos = 1;
+  std::vector<int32_t> radix(n), poff(n);
+  for (int32_t j = 0; j < n; ++j) {
+    const int32_t c = h.comp_class[j];
+    poff[j] = h.cls_pt_off[c];
+    radix[j] = h.cls_pt_off[c + 1] - h.cls_pt_off[c];
+    combos *= radix[j];
+    if (combos > budget) return fail(PB_ERR_BUDGET, "assignment space exceeds the enumeration budget");
+  }
+  if (n > 64) return fail(PB_ERR_UNSUPPORTED, "brute force supports at most 64 computations");
+  std::vector<int64_t> stride(n, 1);
+  for (int32_t j = n - 2; j >= 0; --j) stride[j] = stride[j + 1] * radix[j + 1];
+  // iteration-time range: all fastest .. all slowest (points ascending in time)
+  std::vector<int64_t> lo(n), hi(n);
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t j = h.orig[i];
+    lo[i] = h.pt_time[poff[j]];
+    hi[i] = h.pt_time[poff[j] + radix[j] - 1];
+  }
+  const int64_t t_lo = host_makespan(h, lo), t_hi = host_makespan(h, hi);
+  const int64_t slots = t_hi - t_lo + 1;
+  if (slots > (int64_t{1} << 25)) return fail(PB_ERR_UNSUPPORTED, "iteration-time range too wide to tabulate");
+  return guarded([&]() -> pb_status {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    Blob blob;
+    const size_t o_orig = blob.put(h.orig), o_pinoff = blob.put(h.pin_off), o_pin = blob.put(h.pin),
+                 o_cflag = blob.put(h.cflag), o_stride = blob.put(stride), o_radix = blob.put(radix),
+                 o_poff = blob.put(poff), o_pt = blob.put(h.pt_time), o_pe = blob.put(h.pt_energy);
+    char* d_blob = nullptr;
+    unsigned long long *d_e = nullptr, *d_c = nullptr;
+    pb::DevBrute* d_job = nullptr;
+    ck(cudaMalloc(&d_blob, std::max<size_t>(blob.bytes.size(), 256)), "malloc");
+    ck(cudaMalloc(&d_e, sizeof(unsigned long long) * slots), "malloc");
+    ck(cudaMalloc(&d_c, sizeof(unsigned long long) * slots), "malloc");
+    ck(cudaMalloc(&d_job, sizeof(pb::DevBrute)), "malloc");
+    ck(cudaMemcpy(d_blob, blob.bytes.data(), blob.bytes.size(), cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemset(d_e, 0xff, sizeof(unsigned long long) * slots), "memset");
+    ck(cudaMemset(d_c, 0xff, sizeof(unsigned long long) * slots), "memset");
+    pb::DevBrute J{};
+    J.n = n;
+    J.combos = static_cast<int64_t>(combos);
+    J.t_lo = t_lo;
+    J.slots = slots;
+    J.watts = h.watts;
+    J.quantum = h.quantum;
+    J.orig = dptr<int32_t>(d_blob, o_orig);
+    J.pin_off = dptr<int32_t>(d_blob, o_pinoff);
+    J.pin = dptr<int32_t>(d_blob, o_pin);
+    J.cflag = dptr<uint8_t>(d_blob, o_cflag);
+    J.stride = dptr<int64_t>(d_blob, o_stride);
+    J.radix = dptr<int32_t>(d_blob, o_radix);
+    J.poff = dptr<int32_t>(d_blob, o_poff);
+    J.pt_time = dptr<int64_t>(d_blob, o_pt);
+    J.pt_energy = dptr<int64_t>(d_blob, o_pe);
+    J.best_e = d_e;
+    J.best_code = d_c;
+    ck(cudaMemcpy(d_job, &J, sizeof J, cudaMemcpyHostToDevice), "H2D");
+    for (int pass = 0; pass < 2; ++pass) {
+      const int rc = pb::launch_brute(d_job, J, pass, nullptr);
+      if (rc) throw CudaError(cudaGetErrorString(static_cast<cudaError_t>(rc)));
+    }
+    ck(cudaDeviceSynchronize(), "brute kernel");
+    std::vector<unsigned long long> be(slots), bc(slots);
+    ck(cudaMemcpy(be.data(), d_e, sizeof(unsigned long long) * slots, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(bc.data(), d_c, sizeof(unsigned long long) * slots, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d_blob);
+    cudaFree(d_e);
+    cudaFree(d_c);
+    cudaFree(d_job);
+    // ascending time, strictly decreasing energy (oracle.hpp:96-112)
+    int32_t cnt = 0;
+    bool have = false;
+    double best = 0;
+    for (int64_t s = 0; s < slots; ++s) {
+      if (bc[s] == ~0ull) continue;
+      const unsigned long long key = be[s];
+      const unsigned long long u = (key >> 63) ? (key & ~0x8000000000000000ull) : ~key;
+      double e;
+      std::memcpy(&e, &u, 8);
+      if (have && e >= best) continue;
+      best = e;
+      have = true;
+      if (cnt < capacity && points) {
+        points[cnt] = pb_exact_point{t_lo + s, e, static_cast<int64_t>(bc[s])};
+        if (freq_mhz) {
+          int64_t c = static_cast<int64_t>(bc[s]);
+          for (int32_t j = 0; j < n; ++j) {
+            const int32_t d = static_cast<int32_t>(c / stride[j]);
+            c %= stride[j];
+            freq_mhz[static_cast<size_t>(cnt) * n + j] = h.pt_freq[poff[j] + d];
+          }
+        }
+      }
+      ++cnt;
+    }
+    *count = cnt;
+    return cnt <= capacity || !points ? PB_OK : fail(PB_ERR_INVALID_ARGUMENT, "points buffer too small");
+  });
+}
+
 // ------------------------------------------------------- component kernels
 
 pb_status pb_annotate_slack_batch(int32_t device, int32_t count, const int32_t* n, const int32_t* ne,

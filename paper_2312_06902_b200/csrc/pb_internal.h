@@ -251,6 +251,29 @@ struct DevStraggler {
 int launch_straggler(const DevStraggler* d_jobs, int32_t n_inst, const double* d_factors, int32_t n_factors,
                      int32_t pipelines, pb_savings_row* d_out, void* stream);
 
+// Exhaustive enumeration job (pb_batch_brute_force): internal-order
+// topology + per-computation digit decoding (caller order for the energy sum).
+struct DevBrute {
+  int32_t n, pad;
+  int64_t combos;
+  int64_t t_lo;             // smallest possible iteration time (table origin)
+  int64_t slots;            // table size
+  double watts;
+  int64_t quantum;
+  const int32_t* orig;      // [n] internal -> caller id
+  const int32_t* pin_off;   // [n + 1] internal predecessor CSR
+  const int32_t* pin;
+  const uint8_t* cflag;     // [n] bit 1: edge to the sink
+  const int64_t* stride;    // [n] caller order
+  const int32_t* radix;     // [n] caller order: Pareto points of the class
+  const int32_t* poff;      // [n] caller order: first point of the class
+  const int64_t* pt_time;
+  const int64_t* pt_energy;
+  unsigned long long* best_e;     // [slots] order-preserving key of the best energy
+  unsigned long long* best_code;  // [slots]
+};
+int launch_brute(const DevBrute* d_job, const DevBrute& host_job, int pass, void* stream);
+
 // Host-side launchers (pb_kernels.cu).  slots = number of walker warps (one
 // workspace each).
 // The first n_wide instances of the LPT order (the longest walks, which

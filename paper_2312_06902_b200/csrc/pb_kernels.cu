@@ -34,6 +34,7 @@
 // reference's Edmonds-Karp flow (SURVEY.md §7 parity rule 1).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 
@@ -1483,6 +1484,54 @@ __global__ void straggler_kernel(const DevStraggler* jobs, int n_inst, const dou
   out[g] = r;
 }
 
+// ------------------------------------------------------- exhaustive oracle
+
+constexpr int kBruteMaxN = 64;
+
+// Order-preserving unsigned key of a double (no NaNs here).
+__device__ __forceinline__ unsigned long long dkey(double d) {
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(d));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// One thread per assignment code (oracle.hpp:47-114): iteration time via the
+// longest path in internal (topological) order, effective energy summed in
+// caller index order with explicit round-to-nearest ops (no FMA: the
+// reference's host arithmetic).  Pass 0: best energy per time; pass 1: the
+// smallest code reaching it.
+__global__ void brute_kernel(const DevBrute* jp, int pass) {
+  const DevBrute J = *jp;
+  for (long long code = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; code < J.combos;
+       code += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long t[kBruteMaxN];
+    double eff = 0;
+    for (int j = 0; j < J.n; ++j) {
+      const int d = static_cast<int>((code / J.stride[j]) % J.radix[j]);
+      const long long tj = J.pt_time[J.poff[j] + d];
+      const long long ej = J.pt_energy[J.poff[j] + d];
+      t[j] = tj;
+      // effective_energy_mj (units.hpp:45-48): e - W * t * q * 1e-3
+      const double blk = __dmul_rn(__dmul_rn(__dmul_rn(J.watts, static_cast<double>(tj)), static_cast<double>(J.quantum)), 1e-3);
+      eff = __dadd_rn(eff, __dsub_rn(static_cast<double>(ej), blk));
+    }
+    long long fin[kBruteMaxN];
+    long long ms = 0;
+    for (int i = 0; i < J.n; ++i) {
+      long long st = 0;
+      for (int q = J.pin_off[i]; q < J.pin_off[i + 1]; ++q) st = max(st, fin[J.pin[q]]);
+      fin[i] = st + t[J.orig[i]];
+      if (J.cflag[i] & 2) ms = max(ms, fin[i]);
+    }
+    const long long slot = ms - J.t_lo;
+    if (slot < 0 || slot >= J.slots) continue;  // cannot happen: t_lo / slots bound every path
+    const unsigned long long k = dkey(eff);
+    if (pass == 0)
+      atomicMin(&J.best_e[slot], k);
+    else if (J.best_e[slot] == k)
+      atomicMin(&J.best_code[slot], static_cast<unsigned long long>(code));
+  }
+}
+
 // ------------------------------------------------------------ flow jobs
 
 // max_flow_lower_bounds + min_cut_from_flow on an arbitrary FlowGraph with
@@ -1712,6 +1761,13 @@ int launch_straggler(const DevStraggler* d_jobs, int32_t n_inst, const double* d
   const int total = n_inst * n_factors;
   straggler_kernel<<<(total + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_jobs, n_inst, d_factors,
                                                                                       n_factors, pipelines, d_out);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_brute(const DevBrute* d_job, const DevBrute& host_job, int pass, void* stream) {
+  const long long blocks = std::min<long long>((host_job.combos + 255) / 256, 148LL * 64);
+  brute_kernel<<<static_cast<int>(std::max<long long>(blocks, 1)), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_job, pass);
   return static_cast<int>(cudaGetLastError());
 }
 

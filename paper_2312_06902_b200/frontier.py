@@ -143,6 +143,18 @@ class FrontierBatch:
                                          N.ptr(st, C.c_int32), buf))
         return np.ctypeslib.as_array(buf).copy().reshape(len(self), len(f))
 
+    def brute_force(self, k: int, budget: float = 1e7, device: int = 0):
+        """brute_force_frontier (oracle.hpp:47-114) of instance k on the GPU:
+        (points[time, eff_energy_mj, code], freq_mhz[point, computation])."""
+        n = self._packed[k].n
+        cnt = C.c_int32()
+        N.check(N.lib.pb_batch_brute_force(self._h, k, budget, device, None, None, 0, C.byref(cnt)))
+        pts = (N.ExactPoint * max(cnt.value, 1))()
+        fr = np.zeros(max(cnt.value, 1) * n, np.int32)
+        N.check(N.lib.pb_batch_brute_force(self._h, k, budget, device, pts, N.ptr(fr, C.c_int32), cnt.value,
+                                           C.byref(cnt)))
+        return np.ctypeslib.as_array(pts)[:cnt.value].copy(), fr[:cnt.value * n].reshape(cnt.value, n)
+
     def _text(self, fn, *args) -> str:
         n = C.c_int64()
         N.check(fn(self._h, *args, None, 0, C.byref(n)))

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import paper_2312_06902_b200 as pb
-from paper_2312_06902_b200 import g9
+from paper_2312_06902_b200 import _native as N, g9
 from paper_2312_06902_b200.model import (ClassKey, Computation, CostModel, FrequencyProfile, Kind,
                                          PackedInstance, ProfilePoint, ProfileSet, finalize_custom_dag)
 from oracle import port
@@ -346,3 +346,43 @@ def test_lone_artifacts_match_test_serde_cpp():
         '"t_realized_us":1000,"eff_realized_mj":8925.0,'
         '"computations":[{"id":0,"freq_mhz":1400,"t_planned_us":2000,"e_planned_mj":6708,'
         '"t_realized_us":1000,"e_realized_mj":9000}]}')
+
+
+def test_brute_force_oracle_matches_reference(walks):
+    """pb_batch_brute_force (GPU enumeration) against the reference's
+    brute_force_frontier (tests/golden/brute): identical times, bit-identical
+    effective energies and frequency plans; BudgetExceeded where the reference
+    throws.  Also acceptance gate 1 on the same instances: every frontier
+    point's lookup within 2% of the exact optimum (acceptance.cpp:79-112)."""
+    import struct
+    from conftest import load_golden
+    recs = load_golden("brute.jsonl.gz")
+    b = pb.FrontierBatch()
+    for r in recs:
+        dag, model, tau = instance_from_golden(walks[r["spec"]])
+        b.add(dag, model, tau)
+    b.run(0)
+    checked = 0
+    for k, r in enumerate(recs):
+        if r.get("budget_exceeded"):
+            with pytest.raises(N.BudgetExceeded):
+                b.brute_force(k)
+            continue
+        pts, fr = b.brute_force(k)
+        assert len(pts) == len(r["points"]), r["spec"]
+        for j, ref in enumerate(r["points"]):
+            assert int(pts[j]["time"]) == ref["time"], r["spec"]
+            bits = struct.unpack("<Q", struct.pack("<d", float(pts[j]["eff_energy_mj"])))[0]
+            assert bits == int(ref["eff_bits"]), (r["spec"], j)
+            assert fr[j].tolist() == ref["freq_mhz"], (r["spec"], j)
+        # gate 1: lookup(frontier, exact time) within 2% of the exact optimum
+        s = b.summary(k)
+        tp = b.points(k)["t_planned"]
+        for p in pts:
+            target = min(s.t_star, int(p["time"]))
+            idx = next((q for q in range(s.steps + 1) if tp[q] <= target), s.steps)
+            sched = b.schedule(k, idx)
+            gap = (sched.eff_realized_mj - p["eff_energy_mj"]) / p["eff_energy_mj"]
+            assert gap <= 0.02 + 1e-12, (r["spec"], gap)
+        checked += 1
+    assert checked >= 30
