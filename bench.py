@@ -106,8 +106,11 @@ def build_batch(args, rank, world):
     b = pb.FrontierBatch()
     if args.workload == "batch":
         idx = batch_indices(args.batch, rank, world, args.scaling)
-        for i in idx:
-            b.add_g9(g9.batch_params(i))
+        if idx == list(range(idx[0], idx[0] + len(idx))) if idx else False:
+            b.add_g9_batch(idx[0], len(idx))  # contiguous block: built on all host threads
+        else:
+            for i in idx:
+                b.add_g9(g9.batch_params(i))
         desc = (f"G9 config-5 batch: {args.batch} heterogeneous 1F1B instances per "
                 f"{'GPU' if args.scaling == 'weak' else 'job'} (N 4-16, M 8-256, B=10, imbalance 1.0-1.25, "
                 f"straggler phi in 1.0-1.5), full frontiers, tau=1000us")

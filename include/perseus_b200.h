@@ -274,6 +274,9 @@ pb_status pb_g9_batch_params(int32_t i, int32_t* stages, int32_t* microbatches,
 pb_status pb_batch_add_g9(pb_batch* b, int32_t stages, int32_t microbatches, int32_t base,
                           double imbalance, uint32_t seed, int32_t straggler_stage, double phi,
                           int64_t tau, int32_t* out_index);
+/* Config-5 instances [first, first + count) built in parallel on `threads`
+ * host threads (0 = all), appended in index order. */
+pb_status pb_batch_add_g9_batch(pb_batch* b, int32_t first, int32_t count, int64_t tau, int32_t threads);
 /* The 9 (freq, time, energy) points of a stage base (descending frequency). */
 pb_status pb_g9_profile(int32_t b, int32_t backward, int64_t tau, int32_t* freq, int64_t* time,
                         int64_t* energy);

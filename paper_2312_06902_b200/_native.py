@@ -180,6 +180,7 @@ def _load() -> C.CDLL:
         "pb_batch_profile": (C.c_int, [P, i64p, C.c_int32]),
         "pb_batch_straggler": (C.c_int, [P, C.c_int32, f64p, C.c_int32, i32p, C.POINTER(SavingsRow)]),
         "pb_batch_frontier_csv": (C.c_int, [P, C.c_int32, C.c_int64, C.c_char_p, C.c_int64, i64p]),
+        "pb_batch_add_g9_batch": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, C.c_int32]),
         "pb_batch_brute_force": (C.c_int, [P, C.c_int32, C.c_double, C.c_int32, C.POINTER(ExactPoint), i32p,
                                            C.c_int32, i32p]),
         "pb_batch_schedule_json": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, C.c_char_p, C.c_int64, i64p]),
@@ -212,6 +213,7 @@ EXPORTED = (
     "pb_batch_stats", "pb_batch_profile", "pb_batch_destroy", "pb_annotate_slack_batch", "pb_flow_min_cut_batch",
     "pb_g9_stage_bases", "pb_g9_batch_params", "pb_g9_profile", "pb_batch_add_g9", "pb_batch_straggler",
     "pb_batch_frontier_csv", "pb_batch_schedule_json", "pb_batch_brute_force",
+    "pb_batch_add_g9_batch",
 )
 
 

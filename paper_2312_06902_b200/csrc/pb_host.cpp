@@ -1926,6 +1926,39 @@ pb_status pb_batch_add_g9(pb_batch* b, int32_t stages, int32_t microbatches, int
   return pb_batch_add(b, &d, out_index);
 }
 
+// Config-5 instances [first, first + count) built on all host threads
+// (batched CostModel::build + DAG derivation), appended
+// in index order.
+pb_status pb_batch_add_g9_batch(pb_batch* b, int32_t first, int32_t count, int64_t tau, int32_t threads) {
+  if (!b || first < 0 || count < 0) return fail(PB_ERR_INVALID_ARGUMENT, "bad argument");
+  if (count == 0) return PB_OK;
+  const int32_t nt = std::max(1, std::min<int32_t>(threads > 0 ? threads : static_cast<int32_t>(std::thread::hardware_concurrency()), count));
+  std::vector<pb_batch> parts(nt);
+  std::vector<pb_status> st(nt, PB_OK);
+  std::vector<std::string> err(nt);
+  std::vector<std::thread> pool;
+  const int32_t chunk = (count + nt - 1) / nt;
+  for (int32_t t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      for (int32_t i = first + t * chunk; i < std::min(first + count, first + (t + 1) * chunk); ++i) {
+        const pb_g9::Params q = pb_g9::batch_instance(i);
+        st[t] = pb_batch_add_g9(&parts[t], q.stages, q.microbatches, q.base, q.imbalance, q.seed, q.straggler_stage,
+                                q.phi, tau, nullptr);
+        if (st[t] != PB_OK) {
+          err[t] = g_last_error;
+          return;
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (int32_t t = 0; t < nt; ++t)
+    if (st[t] != PB_OK) return fail(st[t], err[t]);
+  for (auto& part : parts)
+    for (auto& h : part.insts) b->insts.push_back(std::move(h));
+  b->have_results = false;
+  return PB_OK;
+}
+
 pb_status pb_g9_profile(int32_t b, int32_t backward, int64_t tau, int32_t* freq, int64_t* time,
                         int64_t* energy) {
   const auto pts = pb_g9::stage_profile(b, backward != 0, tau);

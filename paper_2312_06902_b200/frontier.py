@@ -143,6 +143,14 @@ class FrontierBatch:
                                          N.ptr(st, C.c_int32), buf))
         return np.ctypeslib.as_array(buf).copy().reshape(len(self), len(f))
 
+    def add_g9_batch(self, first: int, count: int, tau: int = 1000, threads: int = 0) -> None:
+        """Config-5 instances [first, first + count), built on all host threads."""
+        from . import g9
+        N.check(N.lib.pb_batch_add_g9_batch(self._h, first, count, tau, threads))
+        for i in range(first, first + count):
+            p = g9.batch_params(i)
+            self._packed.append(_G9Meta(2 * p.stages * p.microbatches))
+
     def brute_force(self, k: int, budget: float = 1e7, device: int = 0):
         """brute_force_frontier (oracle.hpp:47-114) of instance k on the GPU:
         (points[time, eff_energy_mj, code], freq_mhz[point, computation])."""

@@ -386,3 +386,21 @@ def test_brute_force_oracle_matches_reference(walks):
             assert gap <= 0.02 + 1e-12, (r["spec"], gap)
         checked += 1
     assert checked >= 30
+
+
+def test_parallel_batch_builder_matches_serial_adds():
+    """pb_batch_add_g9_batch (instances built on all host threads) walks
+    exactly like the same instances added one by one."""
+    a = pb.FrontierBatch()
+    a.add_g9_batch(100, 24)
+    c = pb.FrontierBatch()
+    for i in range(100, 124):
+        c.add_g9(g9.batch_params(i))
+    a.run(0)
+    c.run(0)
+    for k in range(24):
+        sa, sc = a.summary(k), c.summary(k)
+        assert (sa.t_min, sa.t_star, sa.steps, sa.stop) == (sc.t_min, sc.t_star, sc.steps, sc.stop)
+        pa, pc = a.points(k), c.points(k)
+        assert pa["t_planned"].tolist() == pc["t_planned"].tolist()
+        assert pa["sum_realized_e"].tolist() == pc["sum_realized_e"].tolist()

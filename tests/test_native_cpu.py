@@ -148,3 +148,12 @@ def test_pareto_filter_matches_oracle():
         mine = pb.pareto_filter([ProfilePoint(a, b, c) for a, b, c in zip(f, t, e)])
         of, ot, oe = port.pareto_filter(f, t, e)
         assert [(p.freq_mhz, p.time, p.energy) for p in mine] == list(zip(of, ot, oe))
+
+
+def test_parallel_batch_builder_counts_and_order():
+    import paper_2312_06902_b200 as pb
+    a = pb.FrontierBatch()
+    a.add_g9_batch(0, 40, threads=3)
+    assert len(a) == 40 and N.lib.pb_batch_size(a._h) == 40
+    with pytest.raises(ValueError):
+        N.check(N.lib.pb_batch_add_g9_batch(a._h, -1, 2, 1000, 0))
