@@ -9,7 +9,8 @@
 //     list carries {other end, twin position, other's list range}, and the
 //     residual of traversing p away from x lives at resid[p].  A BFS level
 //     therefore loads {ient[p], resid[p]} in parallel and nothing else;
-//   * the visited set and the frontier live in shared memory.
+//   * the visited set, the frontier and the last longest-path levels live in
+//     shared memory.
 #pragma once
 
 #include <cstdint>
@@ -136,7 +137,8 @@ enum : int {
   kPrSlots
 };
 
-// Shared memory per walker warp: visited bitset + ping-pong frontier.
+// Shared memory per walker warp: ping-pong BFS frontier, visited and
+// partner-ok bitsets, longest-path rings (layout in pb_kernels.cu bind_ws).
 constexpr int kFrontCap = 128;  // frontier entries per buffer kept in smem
 // Longest-path sweep: values of the last kRingLevels levels (<= 16 per level)
 // also live in a shared-memory ring per direction; a row-record neighbour is

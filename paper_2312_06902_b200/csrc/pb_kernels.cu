@@ -1,10 +1,12 @@
-// sm_100a kernels of the B200-native Perseus frontier generator (v4).
+// sm_100a kernels of the B200-native Perseus frontier generator.
 //
 // One WARP walks one instance's whole frontier (frontier.hpp:166-189) inside
-// a single persistent launch: warps pull instances (LPT order) from a global
-// counter, so thousands of walks are in flight and no host round trip
-// happens per step.  Synchronization is __syncwarp only; appends are ballot
-// compactions.  Per step:
+// a single persistent launch (walk_kernel): warps pull instances (LPT order)
+// from a global counter, so thousands of walks are in flight and no host
+// round trip happens per step.  Synchronization is __syncwarp only; appends
+// are ballot compactions.  The LPT head (the walks that bound the batch)
+// runs in walk_kernel_wide: 2 warps per walk, every BFS level split across
+// them (named barriers).  Per step:
 //
 //   K2  ONE fused longest-path sweep over the level-major computation order:
 //       lanes 0-15 run the forward pass (planned AND realized finish times,
@@ -23,11 +25,17 @@
 //       return arc sink->source (phase A = the feasibility test of
 //       flow.hpp:172-203), then source->sink BFS augmentation (phase B,
 //       flow.hpp:205-228).  A BFS level loads {ient[p], resid[p]} for its
-//       arcs in parallel; the visited set is a shared-memory bitset;
+//       arcs in parallel; the visited set is a shared-memory bitset; a node
+//       reached with a positive computation-arc residual brings its partner
+//       node into the same level (pok bitset), halving BFS depth;
 //   K5  the last phase-B BFS (sink unreachable) marks exactly the source
 //       side of the minimal minimum cut (min_cut_from_flow, flow.hpp:234-262);
 //       tau update with the reference's skip rules (frontier.hpp:111-131),
 //       discretize (frontier.hpp:140-161), append-only delta log.
+//
+// Also here: the component kernels behind pb_flow_min_cut_batch and
+// pb_annotate_slack_batch, the straggler sweep (pb_batch_straggler) and the
+// exhaustive oracle (pb_batch_brute_force).
 //
 // Only the unique minimal min cut and the two verdicts (feasible, value >=
 // sentinel) feed the outputs, so the flow itself is free to differ from the
@@ -1321,7 +1329,8 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.W.dirty = reinterpret_cast<uint8_t*>(base + L.off_ccrit);
   p.W.choice = reinterpret_cast<uint8_t*>(base + L.off_choice);
   p.W.delta = reinterpret_cast<int32_t*>(base + L.off_delta);
-  // shared memory: path ends, frontier (16 B aligned), bitset
+  // shared memory: path ends, frontier (16 B aligned), visited bitset,
+  // partner-ok bitset, longest-path rings
   p.N.ends = reinterpret_cast<int2*>(smem);
   const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   p.N.s_fs = sa + 8 * kMaxEnds;
