@@ -404,3 +404,38 @@ def test_parallel_batch_builder_matches_serial_adds():
         pa, pc = a.points(k), c.points(k)
         assert pa["t_planned"].tolist() == pc["t_planned"].tolist()
         assert pa["sum_realized_e"].tolist() == pc["sum_realized_e"].tolist()
+
+
+def test_batch_scale_invariants():
+    """Size-independent properties on 256 instances of the config-5 batch
+    (N 4-16, M 8-256) in one launch: every G9 walk stops AT_TMIN after
+    ceil((T* - T_min) / tau) steps of exactly tau (last one clipped,
+    acceptance gate 2); the delta log reproduces every point's planned-time
+    sum; ids inside a step are ascending (sped, then slowed); realized
+    iteration times never undercut T_min; the host replay of the last point
+    agrees with the device totals."""
+    b = pb.FrontierBatch()
+    b.add_g9_batch(0, 256)
+    b.run(0)
+    for k in range(len(b)):
+        s = b.summary(k)
+        assert s.status == 0 and pb.STOP_NAMES[s.stop] == "at_t_min", k
+        assert s.steps == -(-(s.t_star - s.t_min) // 1000), k
+        pts = b.points(k)
+        tp = pts["t_planned"]
+        assert tp[0] == s.t_star and tp[-1] == s.t_min
+        assert all(tp[q] - tp[q + 1] == min(1000, tp[q] - s.t_min) for q in range(s.steps)), k
+        assert (pts["t_realized"] >= s.t_min).all()
+        ids, _ = b.deltas(k)
+        for q in range(1, s.steps + 1):
+            p = pts[q]
+            seg = ids[p["id_begin"]:p["id_begin"] + p["n_sped"] + p["n_slowed"]]
+            sp, sl = seg[:p["n_sped"]], -seg[p["n_sped"]:]
+            assert (sp > 0).all() and (sl > 0).all()
+            assert (np.diff(sp) > 0).all() and (np.diff(sl) > 0).all()
+            dt = int(p["sum_planned_t"]) - int(pts[q - 1]["sum_planned_t"])
+            assert dt == int(p["step_size"]) * (len(sl) - len(sp)), (k, q)
+        if k % 32 == 0:
+            last = b.schedule(k, s.steps)
+            assert sum(last.planned_t) == int(pts[-1]["sum_planned_t"])
+            assert sum(last.realized_e) == int(pts[-1]["sum_realized_e"])
