@@ -152,7 +152,7 @@ struct WsLayout {
   int64_t max_n, max_v, max_e;
   int64_t off_resid;                   // int64 [2E] residual by position
   int64_t off_bal;                     // int64 [V] phase-A imbalance
-  int64_t off_log;                     // int4  [V] BFS log {arc, arc before or -1, parent, 0}
+  int64_t off_log;                     // int4  [V] BFS log {arc, arc before or -1, parent, node}
   int64_t off_front;                   // int4  [2V] frontier overflow (ping-pong)
   int64_t off_ecrit;                   // u8    [E] edge critical in the current network
   int64_t off_durp, off_durr;          // int64 [n]
@@ -161,6 +161,8 @@ struct WsLayout {
   int64_t off_cap;                     // int64x2 [n] {lower, upper (-1 = infinite)}
   int64_t off_ccrit, off_choice;       // u8 [n] (off_ccrit: dirty flags)
   int64_t off_touch, off_exl, off_delta, off_path;  // int32 lists
+  int64_t off_pathlog;                 // int32 [V] log entry of each path arc (BFS restart)
+  int64_t off_lvlstart;                // int32 [V + 2] first log index of each BFS level
   int64_t stride;
   int32_t smem_bytes;  // dynamic shared memory per warp
 };
@@ -202,6 +204,8 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   L.off_exl = take(4 * max_v);
   L.off_delta = take(4 * max_n);
   L.off_path = take(4 * max_v);
+  L.off_pathlog = take(4 * max_v);
+  L.off_lvlstart = take(4 * (max_v + 2));
   L.stride = o;
   const int64_t bitwords = (max_v + 31) / 32;
   // frontier, visited bitset, partner-ok bitset, sweep rings (fwd, bwd)

@@ -145,7 +145,10 @@ struct Net {
   const IEnt* ient;
   long long* resid;
   long long* bal;
-  int4* lg;        // BFS log: {arc into the node, arc before it or -1, parent log index, 0}
+  int4* lg;        // BFS log: {arc into the node, arc before it or -1, parent log index, node}
+  int32_t* lvl_start;  // first log index of each BFS level of the last BFS
+  int32_t* path_log;   // per path arc: its log entry (>= 0) or -1 - tail entry (arc into the sink)
+  int last_nlog, last_levels;  // extent of the last BFS (for restarts)
   int4* fglob;     // frontier overflow, 2 buffers of fstride entries
   uint32_t s_bits;  // smem (shared-window address) visited bitset
   uint32_t s_pok;   // smem bitset: node x < 2n whose computation arc to x ^ 1 has residual > 0
@@ -166,6 +169,7 @@ struct Net {
 struct CoopCtl {
   int cmd;   // 0 exit, 1 BFS phase B, 2 BFS phase A
   int nsrc;
+  int start;  // restart level (-1: fresh BFS from the seeds)
   long long S;
   const DevInst* inst;
   int nc[3];                 // next-level sizes, rotating by level
@@ -235,7 +239,7 @@ __device__ __forceinline__ bool bit_of(const Net& N, int u) {
 // Seeds frontier slot k (buffer 0) and log entry k with node v.
 __device__ __forceinline__ void seed(Net& N, int k, int v) {
   fwrite(N, 0, k, make_int4(v, N.inc_off[v], N.inc_off[v + 1], k));
-  N.lg[k] = make_int4(-1 - v, -1, -1, 0);
+  N.lg[k] = make_int4(-1 - v, -1, -1, v);
 }
 
 // Phase B: the arcs of frontier buffer buf (cnt entries) that enter the sink
@@ -289,13 +293,24 @@ __device__ int collect_ends(Net& N, int buf, int cnt) {
 // number of that level's arcs into the sink, recorded in N.ends (0 = sink
 // unreachable; the bitset then marks exactly the residual-reachable set).
 template <bool kA, bool kCoop>
-__device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi) {
+__device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int start) {
   const int ln = lane_id();
   const unsigned lt = lanemask_lt();
   const int nw = kCoop ? N.nw : 1;
   const long long t0 = now();
   const long long negS = -N.S;  // raw residual r is positive iff r != 0 && r >= -S
   int cnt = nsrc, cur = 0, nlog = nsrc, found = -1, levels = 0, prev = 0;
+  if (start >= 0) {
+    // restart: levels <= start are kept from the last BFS, frontier buffer 0
+    // holds level `start` (prepare_restart)
+    levels = start;
+    nlog = N.lvl_start[start + 1];
+    cnt = nlog - N.lvl_start[start];
+  } else if (wi == 0 && ln == 0) {
+    N.lvl_start[0] = 0;
+    N.lvl_start[1] = nsrc;
+  }
+  const int levels0 = levels;
   unsigned arcs = 0, upd = 0;
   tgt = -1;
   const uint32_t snk_word = N.s_bits + 4u * (N.snk >> 5), snk_mask = 1u << (N.snk & 31);
@@ -308,7 +323,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi) {
     const uint32_t fcur = N.s_fs + 16u * kFrontCap * cur, fnxt = N.s_fs + 16u * kFrontCap * nxt;
     int4* gcur = N.fglob + static_cast<size_t>(cur) * N.fstride;
     int4* gnxt = N.fglob + static_cast<size_t>(nxt) * N.fstride;
-    int* ncp = kCoop ? &N.ctl->nc[levels % 3] : nullptr;
+    int* ncp = kCoop ? &N.ctl->nc[levels % 3] : nullptr;  // reset for `levels` done by the poster
     if (kCoop && wi == 0 && ln == 0) N.ctl->nc[(levels + 1) % 3] = 0;
     ++levels;
     int nc = 0;
@@ -352,7 +367,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi) {
         int hitli = -1, hitnode = -1;
         if (c) {
           const int li = nlog + pos;
-          N.lg[li] = make_int4(p, -1, fe.w, 0);
+          N.lg[li] = make_int4(p, -1, fe.w, e.x);
           const int4 ent = make_int4(e.x, e.z, e.w, li);
           // the next level reads this node's arcs: start their DRAM->L1 fill now
           pf_l1(N.ient + e.z);
@@ -371,7 +386,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi) {
           const int zo = (e.x & 1) ? e.z - pd : e.w;
           const int ze = (e.x & 1) ? e.z : e.w + pd;
           const int lz = nlog + posz;
-          N.lg[lz] = make_int4(e.z, p, fe.w, 0);  // y's computation arc, the arc into y, y's parent
+          N.lg[lz] = make_int4(e.z, p, fe.w, z);  // y's computation arc, the arc into y, y's parent
           const int4 ent = make_int4(z, zo, ze, lz);
           pf_l1(N.ient + zo);
           pf_l1(N.resid + zo);
@@ -410,6 +425,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi) {
       __syncwarp();
     }
     nlog += nc;
+    if (wi == 0 && ln == 0) N.lvl_start[levels + 1] = nlog;  // levels was incremented: next level's end
     prev = cnt;
     cnt = nc;
     cur = nxt;
@@ -429,31 +445,68 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi) {
     if (done) break;
   }
   if (kCoop) bar_sync(2, 32 * nw);  // every warp is past its last read of shared state
+  N.last_nlog = nlog;
+  N.last_levels = levels;
   C.arc_scans += arcs;
   C.node_updates += upd;
-  C.add(kPrBfsLevels, levels);
+  C.add(kPrBfsLevels, levels - levels0);
   int ret = found;
   if (!kA) ret = (wi == 0 && (lds32(snk_word) & snk_mask)) ? collect_ends(N, cur ^ 1, prev) : 0;
   C.add(kPrBfs, now() - t0);
   return ret;
 }
 
+// Restart after an augmentation (maximize): every node at BFS level <= j
+// keeps an unsaturated tree path from the source and no new residual arc
+// leaves that set (the augmentation only adds arcs back along its path), so
+// a fresh BFS would repeat levels 0..j exactly.  Un-mark the nodes logged
+// after level j and reload level j into frontier buffer 0.
+__device__ void prepare_restart(Net& N, int j) {
+  const int ln = lane_id();
+  const int b = N.lvl_start[j], e = N.lvl_start[j + 1];
+  for (int i = e + ln; i < N.last_nlog; i += 32) {
+    const int v = N.lg[i].w;
+    atoms_and(N.s_bits + 4u * (v >> 5), ~(1u << (v & 31)));
+  }
+  for (int i = b + ln; i < e; i += 32) {
+    const int v = N.lg[i].w;
+    fwrite(N, 0, i - b, make_int4(v, N.inc_off[v], N.inc_off[v + 1], i));
+  }
+  __syncwarp();
+}
+
 // BFS entry for the walk driver (warp 0): solo, or posted to the CTA's
-// helper warps (walk_kernel_wide) and run cooperatively.
+// helper warps (walk_kernel_wide) and run cooperatively.  start >= 0
+// restarts from that level of the last BFS (prepare_restart).
 template <bool kA>
-__device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
-  if (N.nw <= 1) return bfs_core<kA, false>(N, nsrc, tgt, C, 0);
+__device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C, int start = -1) {
+  if (start >= 0) prepare_restart(N, start);
+  if (N.nw <= 1) return bfs_core<kA, false>(N, nsrc, tgt, C, 0, start);
   if (lane_id() == 0) {
     CoopCtl* k = N.ctl;
     k->cmd = kA ? 2 : 1;
     k->nsrc = nsrc;
+    k->start = start;
     k->S = N.S;
-    k->nc[0] = 0;
+    k->nc[start >= 0 ? start % 3 : 0] = 0;
     k->found = ~0ull;
   }
   __syncwarp();
   bar_sync(1, 32 * N.nw);  // release the helpers
-  return bfs_core<kA, true>(N, nsrc, tgt, C, 0);
+  return bfs_core<kA, true>(N, nsrc, tgt, C, 0, start);
+}
+
+// BFS level of log index i in the last BFS (largest L with lvl_start[L] <= i).
+__device__ __forceinline__ int level_of(const Net& N, int i) {
+  int lo = 0, hi = N.last_levels + 1;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (N.lvl_start[mid] <= i)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
 }
 
 // Pushes flow along a chain: position `first` (if >= 0), then the logged
@@ -463,19 +516,26 @@ __device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C) {
 // bottleneck over the chain's residuals in parallel and updates both sides
 // of every arc.  Returns the amount pushed (0 = chain blocked).
 __device__ long long push_chain(Net& N, int first, int idx, long long cap, bool phaseA, int& src,
-                                Counters& C) {
+                                Counters& C, int* restart = nullptr) {
   const int ln = lane_id();
   int k = 0, s = -1;
   if (ln == 0) {
-    if (first >= 0) N.path[k++] = first;
+    if (first >= 0) {
+      N.path_log[k] = -1 - idx;  // arc into the sink: its tail is entry idx
+      N.path[k++] = first;
+    }
     for (;;) {
       const int4 l = N.lg[idx];
       if (l.x < 0) {
         s = -1 - l.x;
         break;
       }
+      N.path_log[k] = idx;
       N.path[k++] = l.x;
-      if (l.y >= 0) N.path[k++] = l.y;  // shortcut entry: two arcs per hop
+      if (l.y >= 0) {  // shortcut entry: two arcs per hop
+        N.path_log[k] = idx;
+        N.path[k++] = l.y;
+      }
       idx = l.z;
     }
   }
@@ -495,17 +555,30 @@ __device__ long long push_chain(Net& N, int first, int idx, long long cap, bool 
   C.add(kPrPathHops, k);
   if (ln == 0) C.node_updates += 2 * k;
   if (d <= 0) return 0;
+  int jmin = INT_MAX;
   for (int q = ln; q < k; q += 32) {
     const int p = N.path[q];
     const int4 e = ldg_ient(N.ient + p);
     const long long nv = N.resid[p] - d;
     N.resid[p] = nv;
     N.resid[e.y & kTwinMask] += d;
+    const bool sat = eff_res(nv, N.S) <= 0;
     if (e.y & kCompArc) {
       // computation arc owner -> e.x (owner = e.x ^ 1): keep the shortcut bits exact
-      if (eff_res(nv, N.S) <= 0) pok_clear(N, e.x ^ 1);
+      if (sat) pok_clear(N, e.x ^ 1);
       pok_set(N, e.x);
     }
+    if (restart && sat) {
+      // a saturated arc logged at level L (entered a node of level L) leaves
+      // levels <= L - 1 intact; the arc into the sink leaves its tail's level
+      const int pl = N.path_log[q];
+      const int j = pl >= 0 ? level_of(N, pl) - 1 : level_of(N, -1 - pl);
+      jmin = j < jmin ? j : jmin;
+    }
+  }
+  if (restart) {
+    jmin = static_cast<int>(wmin(jmin));
+    *restart = jmin < *restart ? jmin : *restart;
   }
   __syncwarp();
   C.add(kPrPaths, 1);
@@ -528,14 +601,17 @@ __device__ void augment_a(Net& N, int found, int tgt, Counters& C) {
 
 // Phase B augmentation along every recorded end arc into the sink (paths of
 // one BFS level graph; each is re-checked against the current residuals).
-__device__ void augment_b(Net& N, int nend, Counters& C) {
+// Returns the level the next BFS can restart from (-1: none).
+__device__ int augment_b(Net& N, int nend, Counters& C) {
   const long long t0 = now();
+  int restart = INT_MAX;
   for (int k = 0; k < nend; ++k) {
     const int2 en = N.ends[k];
     int src;
-    N.R += push_chain(N, en.x, en.y, LLONG_MAX, false, src, C);
+    N.R += push_chain(N, en.x, en.y, LLONG_MAX, false, src, C, &restart);
   }
   C.add(kPrAugment, now() - t0);
+  return restart == INT_MAX || restart < 0 ? -1 : restart;
 }
 
 // Phase A: repairs the imbalances of the nodes in N.touch (ntouch entries,
@@ -610,18 +686,21 @@ __device__ bool repair(Net& N, int ntouch, Counters& C) {
 // bitset then marks the minimal min cut's source side.
 __device__ void maximize(Net& N, Counters& C) {
   const long long t0 = now();
+  int restart = -1;
   for (;;) {
-    clear_bits(N);
-    if (lane_id() == 0) {
-      test_and_set(N, N.src);
-      seed(N, 0, N.src);
+    if (restart < 0) {
+      clear_bits(N);
+      if (lane_id() == 0) {
+        test_and_set(N, N.src);
+        seed(N, 0, N.src);
+      }
+      __syncwarp();
     }
-    __syncwarp();
     C.add(kPrBfsB, 1);
     int tgt;
-    const int nend = bfs<false>(N, 1, tgt, C);
+    const int nend = bfs<false>(N, 1, tgt, C, restart);
     if (nend <= 0) break;
-    augment_b(N, nend, C);
+    restart = augment_b(N, nend, C);
   }
   C.add(kPrPhaseB, now() - t0);
 }
@@ -1318,6 +1397,10 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.N.fglob = reinterpret_cast<int4*>(base + L.off_front);
   p.N.fstride = static_cast<int>(L.max_v);
   p.N.path = reinterpret_cast<int32_t*>(base + L.off_path);
+  p.N.path_log = reinterpret_cast<int32_t*>(base + L.off_pathlog);
+  p.N.lvl_start = reinterpret_cast<int32_t*>(base + L.off_lvlstart);
+  p.N.last_nlog = 0;
+  p.N.last_levels = 0;
   p.N.touch = reinterpret_cast<int32_t*>(base + L.off_touch);
   p.N.exl = reinterpret_cast<int32_t*>(base + L.off_exl);
   p.W.durp = reinterpret_cast<long long*>(base + L.off_durp);
@@ -1433,11 +1516,12 @@ __global__ void __launch_bounds__(kBlock) walk_kernel_wide(const DevInst* insts,
       N.snk = 2 * I->n + 1;
       N.S = *reinterpret_cast<volatile long long*>(&ctl->S);
       const int nsrc = *reinterpret_cast<volatile int*>(&ctl->nsrc);
+      const int start = *reinterpret_cast<volatile int*>(&ctl->start);
       int tgt;
       if (cmd == 2)
-        bfs_core<true, true>(N, nsrc, tgt, C, wi);
+        bfs_core<true, true>(N, nsrc, tgt, C, wi, start);
       else
-        bfs_core<false, true>(N, nsrc, tgt, C, wi);
+        bfs_core<false, true>(N, nsrc, tgt, C, wi, start);
     }
   }
   flush_counters(C, ctr);
