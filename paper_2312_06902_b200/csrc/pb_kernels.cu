@@ -174,6 +174,11 @@ struct CoopCtl {
   const DevInst* inst;
   int nc[3];                 // next-level sizes, rotating by level
   unsigned long long found;  // phase A: (log index << 32) | node, ~0 = none
+  unsigned long long snk_li; // phase B: log index of the sink's discovery, ~0 = none
+  // Termination is decided per level from log indices (< the level's log
+  // end), never from state a faster warp may already be changing in the
+  // next level -- otherwise warps could leave the level loop at different
+  // levels and deadlock on the barriers.
 };
 
 __device__ __forceinline__ void bar_sync(int id, int nthreads) {
@@ -368,6 +373,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
         if (c) {
           const int li = nlog + pos;
           N.lg[li] = make_int4(p, -1, fe.w, e.x);
+          if (kCoop && !kA && e.x == N.snk) atomicMin(&N.ctl->snk_li, static_cast<unsigned long long>(li));
           const int4 ent = make_int4(e.x, e.z, e.w, li);
           // the next level reads this node's arcs: start their DRAM->L1 fill now
           pf_l1(N.ient + e.z);
@@ -433,12 +439,14 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
     if (kA) {
       if (kCoop) {
         const unsigned long long f = *reinterpret_cast<volatile unsigned long long*>(&N.ctl->found);
-        if (f != ~0ull) {
+        if (f != ~0ull && static_cast<int>(f >> 32) < nlog) {  // a hit of THIS level
           found = static_cast<int>(f >> 32);
           tgt = static_cast<int>(f & 0xffffffffu);
         }
       }
       done = found >= 0;
+    } else if (kCoop) {
+      done = *reinterpret_cast<volatile unsigned long long*>(&N.ctl->snk_li) < static_cast<unsigned long long>(nlog);
     } else {
       done = (lds32(snk_word) & snk_mask) != 0;
     }
@@ -490,6 +498,7 @@ __device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C, int start = -1) {
     k->S = N.S;
     k->nc[start >= 0 ? start % 3 : 0] = 0;
     k->found = ~0ull;
+    k->snk_li = ~0ull;
   }
   __syncwarp();
   bar_sync(1, 32 * N.nw);  // release the helpers
@@ -611,7 +620,11 @@ __device__ int augment_b(Net& N, int nend, Counters& C) {
     N.R += push_chain(N, en.x, en.y, LLONG_MAX, false, src, C, &restart);
   }
   C.add(kPrAugment, now() - t0);
+#ifdef PB_NO_RESTART
+  return -1;
+#else
   return restart == INT_MAX || restart < 0 ? -1 : restart;
+#endif
 }
 
 // Phase A: repairs the imbalances of the nodes in N.touch (ntouch entries,
