@@ -18,6 +18,8 @@ Fixtures (JSON lines, gzip):
 
   artifacts.jsonl.gz  frontier.csv + schedule_<k>.json bytes (serde.hpp:194-257)
   brute.jsonl.gz      brute_force_frontier exact frontiers (oracle.hpp:47-114)
+  walks_large.jsonl.gz  full-size reference walks of G9 configs 3 (8x128) and
+                      4 (16x128) -- ~30 min of reference CPU time ("large")
 
     python tests/golden/make_golden.py [walks|flow|slack|savings|artifacts ...]
   batch_small.jsonl.gz  small config-5 style G9 instances (summaries only)
@@ -52,7 +54,7 @@ SAVINGS_FACTORS = "1.0,1.05,1.1,1.2,1.3,1.5"  # SURVEY §8d config-4 straggler s
 def main():
     if not os.path.exists(DRIVER):
         sys.exit("build the reference driver first: make -C oracle ref")
-    parts = set(sys.argv[1:]) or {"walks", "flow", "slack", "savings", "artifacts", "brute"}
+    parts = set(sys.argv[1:]) or {"walks", "flow", "slack", "savings", "artifacts", "brute"}  # "large": opt-in
     walk_specs = ["diamond", "lone:1000:9000:3000:5000", "lone:1000:9000:3000:5000:800",
                   "lone:1000:5000:11000:800", "config:1", "config:2"]
     walk_specs += [f"grid:{s}:{1 + s % 3}:{1 + s % 4}" for s in range(1, 41)]
@@ -73,6 +75,8 @@ def main():
     if "artifacts" in parts:
         art = ["diamond", "lone:1000:9000:3000:5000", "config:1", "grid:3:1:4", "grid:101:4:3:4", "g9:3:5:9:1.2:7:1:1.5"]
         write("artifacts.jsonl.gz", run("artifacts", "1", *art) + run("artifacts", "10", "config:1", "diamond"))
+    if "large" in parts:
+        write("walks_large.jsonl.gz", run("walkcheck", "config:3") + run("walkcheck", "config:4"))
     if "brute" in parts:
         small = [w for w in walk_specs if w.startswith(("grid:", "diamond", "lone", "cubic:"))][:60]
         write("brute.jsonl.gz", run("brute", *small, "config:1"))

@@ -439,3 +439,21 @@ def test_batch_scale_invariants():
             last = b.schedule(k, s.steps)
             assert sum(last.planned_t) == int(pts[-1]["sum_planned_t"])
             assert sum(last.realized_e) == int(pts[-1]["sum_realized_e"])
+
+
+def test_full_size_configs_3_and_4_bit_exact():
+    """The named full-size configurations against the unmodified reference
+    (tests/golden/walks_large: 8x128 with 3240 steps, 16x128 with 3432 steps;
+    ~30 min of reference CPU time to regenerate): every point's times, cut
+    cost, sped/slowed ids and energies, and every schedule's hash."""
+    from conftest import load_golden
+    recs = load_golden("walks_large.jsonl.gz")
+    b = pb.FrontierBatch()
+    meta = []
+    for w in recs:
+        dag, model, tau = instance_from_golden(w)
+        b.add(dag, model, tau)
+        meta.append(model)
+    b.run(0)
+    for k, (w, model) in enumerate(zip(recs, meta)):
+        check_walk_against(b, k, w, model.blocking_watts, model.quantum_us, full=True)
