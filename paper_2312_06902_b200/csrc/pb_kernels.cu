@@ -149,6 +149,9 @@ struct Net {
   int32_t* lvl_start;  // first log index of each BFS level of the last BFS
   int32_t* path_log;   // per path arc: its log entry (>= 0) or -1 - tail entry (arc into the sink)
   int last_nlog, last_levels;  // extent of the last BFS (for restarts)
+  int32_t* node_li;    // [V] log index of each node marked by the last BFS
+  bool prev_valid;     // the bitset / log / levels still describe the last
+                       // step's final BFS (reach(s) of its max flow)
   int4* fglob;     // frontier overflow, 2 buffers of fstride entries
   uint32_t s_bits;  // smem (shared-window address) visited bitset
   uint32_t s_pok;   // smem bitset: node x < 2n whose computation arc to x ^ 1 has residual > 0
@@ -245,6 +248,7 @@ __device__ __forceinline__ bool bit_of(const Net& N, int u) {
 __device__ __forceinline__ void seed(Net& N, int k, int v) {
   fwrite(N, 0, k, make_int4(v, N.inc_off[v], N.inc_off[v + 1], k));
   N.lg[k] = make_int4(-1 - v, -1, -1, v);
+  N.node_li[v] = k;
 }
 
 // Phase B: the arcs of frontier buffer buf (cnt entries) that enter the sink
@@ -373,6 +377,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
         if (c) {
           const int li = nlog + pos;
           N.lg[li] = make_int4(p, -1, fe.w, e.x);
+          N.node_li[e.x] = li;
           if (kCoop && !kA && e.x == N.snk) atomicMin(&N.ctl->snk_li, static_cast<unsigned long long>(li));
           const int4 ent = make_int4(e.x, e.z, e.w, li);
           // the next level reads this node's arcs: start their DRAM->L1 fill now
@@ -393,6 +398,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
           const int ze = (e.x & 1) ? e.z : e.w + pd;
           const int lz = nlog + posz;
           N.lg[lz] = make_int4(e.z, p, fe.w, z);  // y's computation arc, the arc into y, y's parent
+          N.node_li[z] = lz;
           const int4 ent = make_int4(z, zo, ze, lz);
           pf_l1(N.ient + zo);
           pf_l1(N.resid + zo);
@@ -633,6 +639,8 @@ __device__ int augment_b(Net& N, int nend, Counters& C) {
 // network is infeasible (max_flow_lower_bounds returns nullopt).
 __device__ bool repair(Net& N, int ntouch, Counters& C) {
   const int ln = lane_id();
+  if (ntouch == 0) return true;  // nothing moved: keep the last BFS state
+  N.prev_valid = false;          // the dedup below (and any phase-A BFS) reuses the bitset
   clear_bits(N);
   int nex = 0;
   for (int base = 0; base < ntouch; base += 32) {
@@ -697,9 +705,11 @@ __device__ bool repair(Net& N, int ntouch, Counters& C) {
 
 // Phase B: source->sink augmentation until the sink is unreachable; the
 // bitset then marks the minimal min cut's source side.
-__device__ void maximize(Net& N, Counters& C) {
+// first_restart >= 0: the first BFS resumes the last step's final BFS from
+// that level (build_caps found no residual change below it).
+__device__ void maximize(Net& N, Counters& C, int first_restart = -1) {
   const long long t0 = now();
-  int restart = -1;
+  int restart = N.prev_valid ? first_restart : -1;
   for (;;) {
     if (restart < 0) {
       clear_bits(N);
@@ -715,6 +725,7 @@ __device__ void maximize(Net& N, Counters& C) {
     if (nend <= 0) break;
     restart = augment_b(N, nend, C);
   }
+  N.prev_valid = true;  // the final BFS is complete: reach(s) with its levels
   C.add(kPrPhaseB, now() - t0);
 }
 
@@ -951,9 +962,19 @@ struct CapSums {
 // critical edge keeps its bounds and flow.  Returns PB_OK or
 // PB_ERR_OVERFLOW; ntouch = nodes whose balance moved.
 __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, bool step_changed,
-                          long long ms, CapSums& T, int& ntouch, int* extrap, Counters& C) {
+                          long long ms, CapSums& T, int& ntouch, int* extrap, Counters& C, int& jprev) {
   const int ln = lane_id();
   const int n = I.n;
+  // Level (in the last step's final BFS) below which no residual changes:
+  // every rebuilt edge's endpoints that BFS reached bound it (restart rule
+  // of maximize: a changed arc out of a level-L node leaves levels <= L-1).
+  int jc = INT_MAX;
+  auto touch_level = [&](int node) {
+    if (N.prev_valid && bit_of(N, node)) {
+      const int l = level_of(N, N.node_li[node]) - 1;
+      jc = l < jc ? l : jc;
+    }
+  };
   const long long t0 = now();
   C.add(kPrSteps, 1);
   ntouch = 0;
@@ -1040,6 +1061,8 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
       N.resid[rc.ph] = crit ? fn - l : 0;
       W.cap[i] = make_longlong2(l, inf ? -1 : u);
       W.ecrit[i] = crit;
+      touch_level(2 * i);
+      touch_level(2 * i + 1);
       if (fn != fo) {
         red_add(&N.bal[2 * i + 1], fn - fo);
         red_add(&N.bal[2 * i], fo - fn);
@@ -1084,6 +1107,8 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
         if (crit != oc[q]) {
           const int2 ps = I.epos[n + j];
           W.ecrit[n + j] = crit;
+          touch_level(ec_tail_of(n, uv[q].x));
+          touch_level(ec_head_of(n, uv[q].y));
           if (crit) {
             ++dinf;
             N.resid[ps.y] = 0;
@@ -1121,6 +1146,7 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
   // more than R: infinite edges need clamping only when R exceeds the new
   // sentinel.
   if (N.R > N.S) {
+    N.prev_valid = false;
     const int nedges = n + I.ne;
     for (int base = 0; base < nedges; base += 32) {
       const int k = base + ln;
@@ -1152,6 +1178,8 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
     }
   }
   __syncwarp();
+  jc = static_cast<int>(wmin(jc));
+  jprev = !N.prev_valid ? -1 : (jc == INT_MAX ? N.last_levels - 1 : jc);
   // shortcut bits of the rebuilt computation arcs (exact now that S is known);
   // when a carried flow may reach the sentinel, rebuild them all
   const bool all = N.R >= N.S;
@@ -1183,6 +1211,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   N.ient = I.ient;
   N.S = 0;
   N.R = 0;
+  N.prev_valid = false;
   for (int p = ln; p < 2 * I.E; p += 32) N.resid[p] = 0;
   for (int v = ln; v < I.V; v += 32) N.bal[v] = 0;
   for (int e = ln; e < I.E; e += 32) W.ecrit[e] = 0;
@@ -1253,7 +1282,8 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     int ntouch = 0;
     const bool step_changed = step != prev_step;
     prev_step = step;
-    const int cs = build_caps(I, N, W, step, step_changed, t_cur, sums, ntouch, &bad, C);
+    int jprev = -1;
+    const int cs = build_caps(I, N, W, step, step_changed, t_cur, sums, ntouch, &bad, C, jprev);
     if (cs != PB_OK) {
       status = cs;
       break;
@@ -1263,7 +1293,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       stop = PB_STOP_INFEASIBLE;
       break;
     }
-    maximize(N, C);
+    maximize(N, C, jprev);
     if (N.R >= N.S) {
       stop = PB_STOP_INFINITE_CUT;
       break;
@@ -1414,6 +1444,8 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.N.lvl_start = reinterpret_cast<int32_t*>(base + L.off_lvlstart);
   p.N.last_nlog = 0;
   p.N.last_levels = 0;
+  p.N.node_li = reinterpret_cast<int32_t*>(base + L.off_nodeli);
+  p.N.prev_valid = false;
   p.N.touch = reinterpret_cast<int32_t*>(base + L.off_touch);
   p.N.exl = reinterpret_cast<int32_t*>(base + L.off_exl);
   p.W.durp = reinterpret_cast<long long*>(base + L.off_durp);
