@@ -58,6 +58,7 @@ struct HostInst {
   int32_t n_levels = 0;
   std::vector<int32_t> lvl_off, orig, inv, icls;
   std::vector<uint8_t> cflag;
+  std::vector<int32_t> ilev, snk;  // level of each internal id; ids with an edge to the sink (ascending)
   std::vector<int32_t> pin_off, pin, pout_off, pout;
   std::vector<pb::int4h> frow, brow;
   std::vector<pb::int2h> dep_nd;  // network order (sorted by head, tail)
@@ -210,9 +211,13 @@ pb_status validate_and_derive(HostInst& h) {
   }
   if (n >= (1 << 24)) return fail(PB_ERR_UNSUPPORTED, "more than 2^24 computations");
   // level of each internal id (level-major order)
-  std::vector<int32_t> ilev(n);
+  std::vector<int32_t>& ilev = h.ilev;
+  ilev.assign(n, 0);
   for (int32_t l = 0; l < L; ++l)
     for (int32_t i = h.lvl_off[l]; i < h.lvl_off[l + 1]; ++i) ilev[i] = l;
+  h.snk.clear();
+  for (int32_t i = 0; i < n; ++i)
+    if (h.cflag[i] & 2) h.snk.push_back(i);
   // sweep ring slot of neighbour u seen from i (pb_internal.h kRingLevels)
   auto ring = [&](int32_t i, int32_t u) {
     const int32_t gap = std::abs(ilev[i] - ilev[u]);
@@ -426,7 +431,7 @@ struct Packed {
 enum OffIdx {
   O_ORIG, O_CLASS, O_CFLAG, O_LVLOFF, O_FROW, O_BROW, O_PINOFF, O_PIN, O_POUTOFF, O_POUT, O_DEPND,
   O_INCOFF, O_IENT, O_EPOS, O_DEPORIG, O_CCONST, O_CTMIN, O_CTMAX, O_CTAB, O_CPOFF, O_PTIME, O_PENERGY,
-  O_START, O_CURVE, O_CREC, O_POINTS, O_SUMMARY, O_COUNT
+  O_START, O_CURVE, O_CREC, O_POINTS, O_SUMMARY, O_ILEV, O_SNK, O_COUNT
 };
 
 void put_static(Blob& blob, const HostInst& h, std::array<size_t, 32>& o) {
@@ -445,6 +450,8 @@ void put_static(Blob& blob, const HostInst& h, std::array<size_t, 32>& o) {
   o[O_IENT] = blob.put(h.net.ient);
   o[O_EPOS] = blob.put(h.net.epos);
   o[O_DEPORIG] = blob.put(h.dep_orig);
+  o[O_ILEV] = blob.put(h.ilev);
+  o[O_SNK] = blob.put(h.snk);
 }
 
 void fill_shape(pb::DevInst& d, const HostInst& h) {
@@ -455,6 +462,7 @@ void fill_shape(pb::DevInst& d, const HostInst& h) {
   d.E = h.n + d.ne + 1;
   d.ret_pt = h.net.epos[d.E - 1].x;
   d.ret_ph = h.net.epos[d.E - 1].y;
+  d.n_snk = static_cast<int32_t>(h.snk.size());
 }
 
 // Every static section of instance k in blob order: f(slot, data, bytes).
@@ -478,6 +486,8 @@ void instance_sections(const pb_batch* b, size_t k, bool fill, F&& f) {
   vec(O_IENT, h.net.ient);
   vec(O_EPOS, h.net.epos);
   vec(O_DEPORIG, h.dep_orig);
+  vec(O_ILEV, h.ilev);
+  vec(O_SNK, h.snk);
   vec(O_CCONST, h.cls_const);
   const size_t nc = h.cls_const.size();
   std::vector<int64_t> tmin, tmax;
@@ -640,6 +650,8 @@ void bind_static(pb::DevInst& d, char* base, const std::array<size_t, 32>& o) {
   d.ient = dptr<pb::IEnt>(base, o[O_IENT]);
   d.epos = dptr<int2>(base, o[O_EPOS]);
   d.dep_orig = dptr<int32_t>(base, o[O_DEPORIG]);
+  d.ilev = dptr<int32_t>(base, o[O_ILEV]);
+  d.snk = dptr<int32_t>(base, o[O_SNK]);
 }
 
 void bind_device(Packed& P, char* d_static, char* d_out, size_t tables_off) {
@@ -811,6 +823,25 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   ck(cudaMemsetAsync(R.d_counters, 0, sizeof(pb::RunCounters), R.stream), "memset");
   ck(cudaMemsetAsync(R.d_pool_cursor, 0, sizeof(unsigned long long), R.stream), "memset");
   pb::DeltaPool pool{R.d_pool_ids, R.d_pool_choice, R.d_pool_cursor, R.pool_cap};
+  if (const int mb = env_int("PB_L2_PERSIST_MB", 0); mb > 0 && R.wide.ctas > 0) {
+    int max_persist = 0, max_win = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, R.device);
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, R.device);
+    const size_t persist = std::min<size_t>(static_cast<size_t>(mb) << 20, static_cast<size_t>(max_persist));
+    ck(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist), "persisting L2");
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = R.d_ws;
+    a.accessPolicyWindow.num_bytes = std::min<size_t>(static_cast<size_t>(R.wide.ctas) * R.ws.stride,
+                                                      static_cast<size_t>(max_win));
+    a.accessPolicyWindow.hitRatio =
+        std::min(1.0f, static_cast<float>(persist) / static_cast<float>(a.accessPolicyWindow.num_bytes));
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ck(cudaStreamSetAttribute(R.stream_big, cudaStreamAttributeAccessPolicyWindow, &a), "L2 window");
+    if (std::getenv("PB_L2_VERBOSE"))
+      std::fprintf(stderr, "L2 persist %zu of max %d, window %zu (max %d), hit %.2f\n", persist, max_persist,
+                   a.accessPolicyWindow.num_bytes, max_win, a.accessPolicyWindow.hitRatio);
+  }
   ck(cudaEventRecord(R.ev0, R.stream), "record");
   ck(cudaStreamWaitEvent(R.stream_big, R.ev0, 0), "wait");
   const int rc = pb::launch_walks(R.d_insts, static_cast<int32_t>(N), R.d_order, R.d_counter,

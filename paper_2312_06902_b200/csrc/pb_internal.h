@@ -82,7 +82,7 @@ void build_net(int32_t V, const std::vector<int32_t>& tail, const std::vector<in
 struct DevInst {
   int32_t n, ne, n_levels, mode;
   int32_t max_steps, cap_points, V, E;  // E includes the return arc
-  int32_t ret_pt, ret_ph, pad0, pad1;   // return-arc positions (sink side, source side)
+  int32_t ret_pt, ret_ph, n_snk, pad1;  // return-arc positions (sink side, source side); |snk|
   int64_t tau;
   double watts;
   int64_t quantum;
@@ -91,6 +91,8 @@ struct DevInst {
   const int32_t* comp_class;  // [n]
   const uint8_t* cflag;       // [n] bit 1: has an edge to the sink
   const int32_t* lvl_off;     // [n_levels + 1]
+  const int32_t* ilev;        // [n] level of each computation
+  const int32_t* snk;         // [n_snk] computations with an edge to the sink, ascending
   const int4* frow;           // [n] {count | has-sink << 16, first 3 predecessors (u | ring slot << 24)}
   const int4* brow;           // [n] {count, first 3 successors (same packing)}
   const int32_t* pin_off;     // [n + 1] computation predecessors

@@ -44,6 +44,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 
 #include "pb_internal.h"
@@ -761,32 +762,52 @@ __device__ __forceinline__ longlong2 sweep_val(const longlong2* vals, uint32_t r
 // Fused longest path over the level-major order (K2).  Forward lanes (0-15)
 // compute fin[i] = max over predecessors of fin + (dp[i], dr[i]); backward
 // lanes (16-31, when `back`) compute tl[i].x = dp[i] + max over successors
-// tl.x.  Level k of the forward pass and level L-1-k of the backward pass run
-// in the same iteration.  The per-level static data (row records, level
-// bounds) and the durations are loaded one iteration ahead.
+// tl.x.  The forward pass covers levels lf..L-1 and the backward pass levels
+// lb..0, one level of each per iteration: a walk step changes durations only
+// at the computations it sped up or slowed down, so fin is unchanged below
+// the lowest of their levels and tl above the highest (lf = 0, lb = L - 1 is
+// the full sweep).  The per-level static data (row records, level bounds) and
+// the durations are loaded one iteration ahead.
 __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr, longlong2* fin,
                       longlong2* tl, bool back, long long& msp, long long& msr, uint32_t s_ring,
-                      Counters& C) {
+                      Counters& C, int lf = 0, int lb = INT_MAX) {
   const int ln = lane_id();
   const long long t0 = now();
   const bool fwd = ln < 16;
   const int s = ln & 15;
   const int L = I.n_levels;
-  const bool active = fwd || back;
+  if (lb > L - 1) lb = L - 1;
+  if (!back) lb = -1;
+  const int nf = L - lf, nb = lb + 1;
+  const int cnt_me = fwd ? nf : nb;  // levels of this half
+  const int iters = max(nf, nb);
   const int4* row = fwd ? I.frow : I.brow;
   const int32_t* noff = fwd ? I.pin_off : I.pout_off;
-  const int32_t* nb = fwd ? I.pin : I.pout;
+  const int32_t* nb_ = fwd ? I.pin : I.pout;
   longlong2* vals = fwd ? fin : tl;
   const uint32_t ring = (fwd ? s_ring : s_ring + 16u * kRingLevels * 16);
   long long mp = 0, mr = 0;
-  C.add(kPrLpLevels, L);
-  auto lev_of = [&](int k) { return fwd ? k : L - 1 - k; };
+  C.add(kPrLpLevels, iters);
+  auto lev_of = [&](int k) { return fwd ? lf + k : lb - k; };
+  // the levels just outside the swept range keep their values: reload their
+  // ring slots (row records name ring slots up to kRingLevels - 1 levels away)
+  if (fwd ? lf > 0 : (back && lb < L - 1)) {
+    for (int d = 1; d < kRingLevels; ++d) {
+      const int lev = fwd ? lf - d : lb + d;
+      if (lev < 0 || lev >= L || cnt_me <= 0) continue;
+      const int b = I.lvl_off[lev], e = I.lvl_off[lev + 1];
+      if (b + s < e) {
+        const longlong2 v = vals[b + s];
+        sts_ll2(ring + 16u * ((lev % kRingLevels) * 16 + s), v.x, v.y);
+      }
+    }
+  }
   int b0 = 0, e0 = 0, b1 = 0, e1 = 0;
-  if (active && L > 0) {
+  if (cnt_me > 0) {
     b0 = I.lvl_off[lev_of(0)];
     e0 = I.lvl_off[lev_of(0) + 1];
   }
-  if (active && L > 1) {
+  if (cnt_me > 1) {
     b1 = I.lvl_off[lev_of(1)];
     e1 = I.lvl_off[lev_of(1) + 1];
   }
@@ -797,11 +818,12 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
     dp0 = dp[b0 + s];
     dr0 = fwd ? dr[b0 + s] : 0;
   }
-  int pf = fwd ? 0 : I.n;  // next row not yet prefetched (this half's direction)
-  for (int k = 0; k < L; ++k) {
+  int pf = fwd ? b0 : e0;  // next row not yet prefetched (this half's direction)
+  __syncwarp();
+  for (int k = 0; k < iters; ++k) {
     // issue the loads of the next iterations
     int b2 = 0, e2 = 0;
-    if (active && k + 2 < L) {
+    if (k + 2 < cnt_me) {
       b2 = I.lvl_off[lev_of(k + 2)];
       e2 = I.lvl_off[lev_of(k + 2) + 1];
     }
@@ -824,13 +846,13 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
       y = max(max(v0.y, v1.y), max(v2.y, y));
       if (cnt > 3)
         for (int j = noff[i0] + 3; j < noff[i0 + 1]; ++j) {
-          const longlong2 v = vals[nb[j]];
+          const longlong2 v = vals[nb_[j]];
           x = max(x, v.x);
           y = max(y, v.y);
         }
       const long long a = x + dp0, c = fwd ? y + dr0 : 0;
       vals[i0] = make_longlong2(a, c);
-      if (s < 16) sts_ll2(ring + 16u * ((lev_of(k) % kRingLevels) * 16 + s), a, c);
+      sts_ll2(ring + 16u * ((lev_of(k) % kRingLevels) * 16 + s), a, c);
       if (fwd && (r0.x >> 16)) {
         mp = max(mp, a);
         mr = max(mr, c);
@@ -840,7 +862,7 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
       for (int i = i0 + 16; i < e0; i += 16) {
         long long xx = 0, yy = 0;
         for (int j = noff[i]; j < noff[i + 1]; ++j) {
-          const longlong2 v = vals[nb[j]];
+          const longlong2 v = vals[nb_[j]];
           xx = max(xx, v.x);
           yy = max(yy, v.y);
         }
@@ -855,7 +877,7 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
     }
     // each row / duration line prefetched once, ~64 computations ahead
     // (level-major order: the sweep consumes them contiguously)
-    if (active) {
+    if (k < cnt_me) {
       if (fwd) {
         const int want = min(b0 + 64, I.n);
         if (pf < want) {
@@ -887,6 +909,17 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
     r0 = r1;
     dp0 = dp1;
     dr0 = dr1;
+  }
+  // sink computations below the forward range keep their finish times
+  if (lf > 0) {
+    const int lim = lf < L ? I.lvl_off[lf] : I.n;
+    for (int j = ln; j < I.n_snk; j += 32) {
+      const int i = I.snk[j];
+      if (i >= lim) break;
+      const longlong2 v = fin[i];
+      mp = max(mp, v.x);
+      mr = max(mr, v.y);
+    }
   }
   msp = wmax(mp);
   msr = wmax(mr);
@@ -1373,6 +1406,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       pool.choice[at + rank] = static_cast<uint8_t>(chnew);
     }
     __syncwarp();
+    int imin = INT_MAX, imax = -1;
     for (int q = ln; q < nd; q += 32) {
       const int x = W.delta[q];
       const int i = (x > 0 ? x : -x) - 1;
@@ -1383,7 +1417,11 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       W.choice[i] = static_cast<uint8_t>(ch);
       W.durr[i] = I.pt_time[I.cls_pt_off[c] + ch];
       W.dirty[i] = 1;
+      imin = min(imin, i);
+      imax = max(imax, i);
     }
+    imin = __reduce_min_sync(kFull, imin);
+    imax = __reduce_max_sync(kFull, imax);
     __syncwarp();
     const int ns = static_cast<int>(wsum(ns_loc));
     dpe = wsum(dpe);
@@ -1394,7 +1432,9 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     // refresh_totals (frontier.hpp:64-67) + discretize (frontier.hpp:157):
     // planned and realized makespans and the next step's tails, one sweep
     long long t_new;
-    sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_new, t_real, N.s_ring, C);
+    // computation ids are level-major: levels below imin's keep fin, above imax's keep tl
+    const int lf = nd ? I.ilev[imin] : I.n_levels, lb = nd ? I.ilev[imax] : -1;
+    sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_new, t_real, N.s_ring, C, lf, lb);
     if (I.mode == kModeDiscover && t_new >= t_cur) {
       stop = PB_STOP_NO_PROGRESS;
       break;
@@ -1862,6 +1902,8 @@ size_t block_smem(const WsLayout& L) {
 template <class K>
 void set_smem(K kernel, size_t bytes) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (const char* e = std::getenv("PB_CARVEOUT"))
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e));
 }
 
 }  // namespace

@@ -7,8 +7,8 @@ mkdir -p gpurun_out
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_bench.log 2>&1
 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,sm__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active,l1tex__t_sector_hit_rate.pct,lts__t_sector_hit_rate.pct \
-  --clock-control none -k regex:walk_kernel -c 1 --csv --log-file gpurun_out/walk_metrics.csv \
+  --clock-control none -k regex:"walk_kernel$" -c 1 --csv --log-file gpurun_out/walk_metrics.csv \
   python tools/walk_profile.py batch:4096 > gpurun_out/ncu_metrics.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:walk_kernel -c 1 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"walk_kernel$" -c 1 \
   -o gpurun_out/walk_full python tools/walk_profile.py ${NCU_CASE:-config2*1776} > gpurun_out/ncu_full.log 2>&1
 tail -2 gpurun_out/ncu_full.log

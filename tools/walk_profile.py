@@ -59,6 +59,8 @@ def profile(name):
             heapq.heappush(slots, t + us)
         print(f"   walks: longest {walks[0][0] / 1e3:.1f} ms, median {walks[len(walks) // 2][0] / 1e3:.2f} ms, "
               f"sum {sum(w for w, _ in walks) / 1e6:.1f} s; LPT replay makespan {max(slots) / 1e3:.1f} ms")
+        print("   top walks (ms, index, steps): " + ", ".join(
+            f"{us / 1e3:.0f}/{k}/{b.summary(k).steps}" for us, k in walks[:8]))
     if bad:
         print("   FAILED (index, status, detail, steps):", bad[:10])
 
