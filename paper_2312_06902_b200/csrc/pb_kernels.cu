@@ -535,11 +535,11 @@ __device__ long long push_chain(Net& N, int first, int idx, long long cap, bool 
                                 Counters& C, int* restart = nullptr) {
   const int ln = lane_id();
   int k = 0, s = -1;
+  if (ln == 0 && first >= 0) {
+    N.path_log[k] = -1 - idx;  // arc into the sink: its tail is entry idx
+    N.path[k++] = first;
+  }
   if (ln == 0) {
-    if (first >= 0) {
-      N.path_log[k] = -1 - idx;  // arc into the sink: its tail is entry idx
-      N.path[k++] = first;
-    }
     for (;;) {
       const int4 l = N.lg[idx];
       if (l.x < 0) {
@@ -752,13 +752,6 @@ __device__ __forceinline__ longlong2 lds_ll2(uint32_t a) {
   asm volatile("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a) : "memory");
   return v;
 }
-// Neighbour value for the sweep: shared ring slot when the row record has
-// one (neighbour at most kRingLevels - 1 levels away), else global memory.
-__device__ __forceinline__ longlong2 sweep_val(const longlong2* vals, uint32_t ring, int packed) {
-  const unsigned slot = static_cast<unsigned>(packed) >> 24;
-  return slot != kRingNone ? lds_ll2(ring + 16u * slot) : vals[packed & 0xffffff];
-}
-
 // Fused longest path over the level-major order (K2).  Forward lanes (0-15)
 // compute fin[i] = max over predecessors of fin + (dp[i], dr[i]); backward
 // lanes (16-31, when `back`) compute tl[i].x = dp[i] + max over successors
@@ -838,12 +831,33 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
     if (i0 < e0) {
       const int cnt = r0.x & 0xffff;
       long long x = 0, y = 0;
+      // ring reads first (shared memory only); the rare far neighbours
+      // (global memory) are folded in by a separate, normally skipped block
+      const unsigned q0 = static_cast<unsigned>(r0.y) >> 24, q1 = static_cast<unsigned>(r0.z) >> 24,
+                     q2 = static_cast<unsigned>(r0.w) >> 24;
+      const bool g0 = cnt > 0 && q0 == kRingNone, g1 = cnt > 1 && q1 == kRingNone, g2 = cnt > 2 && q2 == kRingNone;
       longlong2 v0 = make_longlong2(0, 0), v1 = v0, v2 = v0;
-      if (cnt > 0) v0 = sweep_val(vals, ring, r0.y);
-      if (cnt > 1) v1 = sweep_val(vals, ring, r0.z);
-      if (cnt > 2) v2 = sweep_val(vals, ring, r0.w);
+      if (cnt > 0 && !g0) v0 = lds_ll2(ring + 16u * q0);
+      if (cnt > 1 && !g1) v1 = lds_ll2(ring + 16u * q1);
+      if (cnt > 2 && !g2) v2 = lds_ll2(ring + 16u * q2);
       x = max(max(v0.x, v1.x), max(v2.x, x));
       y = max(max(v0.y, v1.y), max(v2.y, y));
+      if (g0 | g1 | g2) {
+        const int m = g0 ? r0.y : (g1 ? r0.z : r0.w);
+        const longlong2 v = vals[m & 0xffffff];
+        x = max(x, v.x);
+        y = max(y, v.y);
+        if (g0 && g1) {
+          const longlong2 w = vals[r0.z & 0xffffff];
+          x = max(x, w.x);
+          y = max(y, w.y);
+        }
+        if (g2 && (g0 || g1)) {
+          const longlong2 w = vals[r0.w & 0xffffff];
+          x = max(x, w.x);
+          y = max(y, w.y);
+        }
+      }
       if (cnt > 3)
         for (int j = noff[i0] + 3; j < noff[i0 + 1]; ++j) {
           const longlong2 v = vals[nb_[j]];
