@@ -1027,7 +1027,10 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
   ntouch = 0;
   i128 dl = 0, du = 0;
   long long dinf = 0;
-  constexpr int kU = 4;
+#ifndef PB_CAP_KU
+#define PB_CAP_KU 4
+#endif
+  constexpr int kU = PB_CAP_KU;
   // stage 1: criticality of every computation, heavy ones compacted into W.delta
   int nh = 0;
   for (int base = 0; base < n; base += 32 * kU) {
