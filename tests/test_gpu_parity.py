@@ -135,6 +135,61 @@ def test_random_g9_instances_vs_oracle():
         assert last.planned_t == ref["final_planned_t"] and last.freq_mhz == ref["final_freq"]
 
 
+def _layered_dag(rng, levels, max_width, stages):
+    """Random layered DAG: levels wider than 16, up to 6 predecessors (some
+    more than 3 levels back) and computations without successors at every
+    level, so the sweep's overflow rows, far neighbours and the makespan over
+    sinks below an incremental forward range are all exercised."""
+    comps, edges, by_level = [], [], []
+    for lev in range(levels):
+        ids = []
+        for _ in range(int(rng.integers(1, max_width + 1))):
+            i = len(comps)
+            comps.append(Computation(i, int(rng.integers(0, stages)), i, Kind(int(rng.integers(0, 2)))))
+            ids.append(i)
+            if lev:
+                preds = {int(rng.choice(by_level[lev - 1]))}
+                for _ in range(int(rng.integers(0, 6))):
+                    lv = int(rng.integers(max(0, lev - 8), lev))
+                    preds.add(int(rng.choice(by_level[lv])))
+                edges += [(u, i) for u in sorted(preds)]
+        by_level.append(ids)
+    ps = ProfileSet(75.0, [])
+    for s in range(stages):
+        b = int(rng.integers(8, 13))
+        ps.profiles.append(FrequencyProfile(ClassKey(s, int(Kind.Forward)), g9.stage_profile(b, False)))
+        ps.profiles.append(FrequencyProfile(ClassKey(s, int(Kind.Backward)), g9.stage_profile(b, True)))
+    return finalize_custom_dag(comps, edges), CostModel.build(ps)
+
+
+def test_layered_dags_incremental_sweep_vs_oracle():
+    """Walks on irregular DAGs (wide levels, deep fan-in, early sinks) against
+    the C oracle: every makespan, cut cost and the final plan bit-exact."""
+    rng = np.random.default_rng(2024)
+    b = pb.FrontierBatch()
+    packs = []
+    for k in range(12):
+        dag, model = _layered_dag(rng, int(rng.integers(4, 30)), 24 if k % 2 else 6, 3)
+        b.add(dag, model, g9.TAU)
+        packs.append(PackedInstance(dag, model, g9.TAU))
+    b.run(0)
+    sinks = 0
+    for k, P in enumerate(packs):
+        ref = port.discover_frontier(P, g9.TAU)
+        s = b.summary(k)
+        pts = b.points(k)
+        assert s.status == 0
+        assert s.steps == ref["steps"] and pb.STOP_NAMES[s.stop] == ref["reason"]
+        assert pts["t_planned"].tolist() == ref["t_planned"]
+        assert pts["t_realized"].tolist() == ref["t_realized"]
+        assert pts["cut_cost"][1:].tolist() == ref["cut_cost"]
+        last = b.schedule(k, s.steps)
+        assert last.planned_t == ref["final_planned_t"] and last.freq_mhz == ref["final_freq"]
+        sinks += int(np.count_nonzero(P.edge_head == P.n + 1) > 1)
+    assert sinks >= 6  # several sink computations per DAG
+    assert sum(b.summary(k).steps for k in range(len(packs))) > 100
+
+
 # ---- the reference API, test_frontier.cpp style -----------------------------
 
 def _lone(ft, fe, st, se):
