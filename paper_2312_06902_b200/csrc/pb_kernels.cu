@@ -168,10 +168,11 @@ struct Net {
   int nw;
 };
 
+constexpr int kCtlBytes = 256;  // shared memory reserved for CoopCtl
 // Control block of a cooperative walk CTA (shared memory): warp 0 drives the
 // walk and posts each BFS as a job; helper warps join it.
 struct CoopCtl {
-  int cmd;   // 0 exit, 1 BFS phase B, 2 BFS phase A
+  int cmd;   // 0 exit, 1 BFS phase B, 2 BFS phase A, 3 capacity-pass dependency edges
   int nsrc;
   int start;  // restart level (-1: fresh BFS from the seeds)
   long long S;
@@ -179,6 +180,12 @@ struct CoopCtl {
   int nc[3];                 // next-level sizes, rotating by level
   unsigned long long found;  // phase A: (log index << 32) | node, ~0 = none
   unsigned long long snk_li; // phase B: log index of the sink's discovery, ~0 = none
+  // cmd 3 (capacity pass, dependency edges): inputs and per-warp results
+  long long ms;
+  int ntouch;       // shared touch-list length
+  int prev_valid, last_levels;
+  int part_jc[4];
+  long long part_dinf[4];
   // Termination is decided per level from log indices (< the level's log
   // end), never from state a faster warp may already be changing in the
   // next level -- otherwise warps could leave the level loop at different
@@ -1003,6 +1010,99 @@ struct CapSums {
   long long ninf;
 };
 
+#ifndef PB_CAP_KU
+#define PB_CAP_KU 4  // blocks of 32 * PB_CAP_KU computations / edges per round
+#endif
+
+// Dependency edges of build_caps (always infinite, lower bound 0): only
+// criticality changes matter.  Warp wi of nw takes every nw-th block of
+// 32 * kU edges; kCoop appends to the touch list through the CTA's shared
+// counter (N.ctl->ntouch) instead of the warp-local count.
+template <bool kCoop>
+__device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int wi, int& ntouch,
+                          long long& dinf, int& jc) {
+  const int ln = lane_id();
+  const int n = I.n;
+  const int nw = kCoop ? N.nw : 1;
+  constexpr int kU = PB_CAP_KU;
+  auto touch_level = [&](int node) {
+    if (N.prev_valid && bit_of(N, node)) {
+      const int l = level_of(N, N.node_li[node]) - 1;
+      jc = l < jc ? l : jc;
+    }
+  };
+  for (int base = 32 * kU * wi; base < I.ne; base += 32 * kU * nw) {
+    int2 uv[kU];
+    bool oc[kU], tc[kU], hc[kU];
+    long long te[kU], he[kU], hd[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int j = min(base + 32 * q + ln, I.ne - 1);
+      uv[q] = I.dep_nd[j];
+      oc[q] = W.ecrit[n + j];
+    }
+    // endpoint loads, branch-free (index 0 stands in for the source / sink)
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const bool ts = uv[q].x == n, hs = uv[q].y == n + 1;
+      const int tu = ts ? 0 : uv[q].x, hv = hs ? 0 : uv[q].y;
+      const bool tcr = W.ecrit[tu], hcr = W.ecrit[hv];
+      const long long tf = W.fin[tu].x, hf = W.fin[hv].x, hdd = W.durp[hv];
+      tc[q] = ts || tcr;
+      hc[q] = hs || hcr;
+      te[q] = ts ? 0 : tf;
+      he[q] = hs ? ms : hf;
+      hd[q] = hs ? 0 : hdd;
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int j = base + 32 * q + ln;
+      bool ch = false;
+      int et = 0, eh = 0;
+      if (j < I.ne) {
+        const bool crit = tc[q] && hc[q] && te[q] == he[q] - hd[q];
+        if (crit != oc[q]) {
+          const int2 ps = I.epos[n + j];
+          W.ecrit[n + j] = crit;
+          touch_level(ec_tail_of(n, uv[q].x));
+          touch_level(ec_head_of(n, uv[q].y));
+          if (crit) {
+            ++dinf;
+            N.resid[ps.y] = 0;
+            N.resid[ps.x] = -1;  // infinite forward side carrying f = 0
+          } else {
+            --dinf;
+            const long long fo = N.resid[ps.y];
+            N.resid[ps.y] = 0;
+            N.resid[ps.x] = 0;
+            if (fo != 0) {
+              et = ec_tail_of(n, uv[q].x);
+              eh = ec_head_of(n, uv[q].y);
+              red_add(&N.bal[eh], -fo);
+              red_add(&N.bal[et], fo);
+              ch = true;
+            }
+          }
+        }
+      }
+      if (kCoop) {
+        // shared append: both endpoints of each changed edge, adjacent
+        const unsigned bm = __ballot_sync(kFull, ch);
+        int at = 0;
+        if (ln == 0 && bm) at = atomicAdd(&N.ctl->ntouch, 2 * __popc(bm));
+        at = __shfl_sync(kFull, at, 0) + 2 * __popc(bm & lanemask_lt());
+        if (ch) {
+          N.touch[at] = et;
+          N.touch[at + 1] = eh;
+        }
+      } else {
+        wappend(ch, et, N.touch, ntouch);
+        wappend(ch, eh, N.touch, ntouch);
+      }
+    }
+  }
+}
+
 // K3: critical mask + Eq. 7 capacities + warm-start clamp.  Only "heavy"
 // edges are rebuilt: those whose criticality changed, and critical
 // computations whose duration (dirty) or the step size changed; every other
@@ -1027,9 +1127,6 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
   ntouch = 0;
   i128 dl = 0, du = 0;
   long long dinf = 0;
-#ifndef PB_CAP_KU
-#define PB_CAP_KU 4
-#endif
   constexpr int kU = PB_CAP_KU;
   // stage 1: criticality of every computation, heavy ones compacted into W.delta
   int nh = 0;
@@ -1124,63 +1221,28 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
   }
   __syncwarp();
   // dependency edges (always infinite, lower bound 0): only criticality changes matter
-  for (int base = 0; base < I.ne; base += 32 * kU) {
-    int2 uv[kU];
-    bool oc[kU], tc[kU], hc[kU];
-    long long te[kU], he[kU], hd[kU];
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int j = min(base + 32 * q + ln, I.ne - 1);
-      uv[q] = I.dep_nd[j];
-      oc[q] = W.ecrit[n + j];
+  if (N.nw > 1) {
+    // cooperative walk: the helper warps take every nw-th block of edges
+    if (ln == 0) {
+      CoopCtl* k = N.ctl;
+      k->cmd = 3;
+      k->ms = ms;
+      k->ntouch = ntouch;
+      k->prev_valid = N.prev_valid;
+      k->last_levels = N.last_levels;
     }
-    // endpoint loads, branch-free (index 0 stands in for the source / sink)
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const bool ts = uv[q].x == n, hs = uv[q].y == n + 1;
-      const int tu = ts ? 0 : uv[q].x, hv = hs ? 0 : uv[q].y;
-      const bool tcr = W.ecrit[tu], hcr = W.ecrit[hv];
-      const long long tf = W.fin[tu].x, hf = W.fin[hv].x, hdd = W.durp[hv];
-      tc[q] = ts || tcr;
-      hc[q] = hs || hcr;
-      te[q] = ts ? 0 : tf;
-      he[q] = hs ? ms : hf;
-      hd[q] = hs ? 0 : hdd;
+    __syncwarp();
+    bar_sync(1, 32 * N.nw);  // release the helpers
+    dep_edges<true>(I, N, W, ms, 0, ntouch, dinf, jc);
+    bar_sync(2, 32 * N.nw);  // every warp's edges are done
+    ntouch = *reinterpret_cast<volatile int*>(&N.ctl->ntouch);
+    for (int w = 1; w < N.nw; ++w) {
+      dinf += ln == 0 ? *reinterpret_cast<volatile long long*>(&N.ctl->part_dinf[w]) : 0;
+      const int j = *reinterpret_cast<volatile int*>(&N.ctl->part_jc[w]);
+      jc = j < jc ? j : jc;
     }
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int j = base + 32 * q + ln;
-      bool ch = false;
-      int et = 0, eh = 0;
-      if (j < I.ne) {
-        const bool crit = tc[q] && hc[q] && te[q] == he[q] - hd[q];
-        if (crit != oc[q]) {
-          const int2 ps = I.epos[n + j];
-          W.ecrit[n + j] = crit;
-          touch_level(ec_tail_of(n, uv[q].x));
-          touch_level(ec_head_of(n, uv[q].y));
-          if (crit) {
-            ++dinf;
-            N.resid[ps.y] = 0;
-            N.resid[ps.x] = -1;  // infinite forward side carrying f = 0
-          } else {
-            --dinf;
-            const long long fo = N.resid[ps.y];
-            N.resid[ps.y] = 0;
-            N.resid[ps.x] = 0;
-            if (fo != 0) {
-              et = ec_tail_of(n, uv[q].x);
-              eh = ec_head_of(n, uv[q].y);
-              red_add(&N.bal[eh], -fo);
-              red_add(&N.bal[et], fo);
-              ch = true;
-            }
-          }
-        }
-      }
-      wappend(ch, et, N.touch, ntouch);
-      wappend(ch, eh, N.touch, ntouch);
-    }
+  } else {
+    dep_edges<false>(I, N, W, ms, 0, ntouch, dinf, jc);
   }
   T.suml += wsum128(dl);
   T.sumu += wsum128(du);
@@ -1581,7 +1643,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel(const DevInst*
 // posted to the CTA's control block and expanded by all nw warps
 // (bfs_core<., true>); the other phases stay on warp 0.  The walk's shared
 // structures (frontier, bitsets, path ends) are warp 0's region.
-__global__ void __launch_bounds__(kBlock) walk_kernel_wide(const DevInst* insts, int n_wide,
+__global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel_wide(const DevInst* insts, int n_wide,
                                                            const int32_t* order, int32_t* counter,
                                                            char* ws_base, WsLayout L, RunCounters* ctr,
                                                            DeltaPool pool) {
@@ -1614,6 +1676,22 @@ __global__ void __launch_bounds__(kBlock) walk_kernel_wide(const DevInst* insts,
       if (cmd == 0) break;
       const DevInst* I = *reinterpret_cast<const DevInst* volatile*>(&ctl->inst);
       Net& N = P.N;
+      if (cmd == 3) {
+        // capacity pass: this warp's blocks of dependency edges
+        N.prev_valid = *reinterpret_cast<volatile int*>(&ctl->prev_valid) != 0;
+        N.last_levels = *reinterpret_cast<volatile int*>(&ctl->last_levels);
+        long long dinf = 0;
+        int jc = INT_MAX, unused = 0;
+        dep_edges<true>(*I, N, P.W, *reinterpret_cast<volatile long long*>(&ctl->ms), wi, unused, dinf, jc);
+        dinf = wsum(dinf);
+        jc = static_cast<int>(wmin(jc));
+        if (lane_id() == 0) {
+          ctl->part_dinf[wi] = dinf;
+          ctl->part_jc[wi] = jc;
+        }
+        bar_sync(2, 32 * nw);
+        continue;
+      }
       N.ient = I->ient;
       N.snk = 2 * I->n + 1;
       N.S = *reinterpret_cast<volatile long long*>(&ctl->S);
@@ -1939,7 +2017,8 @@ int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order,
                  DeltaPool pool, int32_t n_wide, int32_t wide_ctas, int32_t wide_warps, void* stream,
                  void* stream_wide) {
   if (n_wide > 0 && wide_ctas > 0) {
-    const size_t sm = static_cast<size_t>(wide_warps) * (128 + 8 * kMaxEnds + ws.smem_bytes) + 128;
+    static_assert(sizeof(CoopCtl) <= kCtlBytes, "CoopCtl outgrew its shared-memory block");
+    const size_t sm = static_cast<size_t>(wide_warps) * (128 + 8 * kMaxEnds + ws.smem_bytes) + kCtlBytes;
     set_smem(walk_kernel_wide, sm);
     walk_kernel_wide<<<wide_ctas, 32 * wide_warps, sm, static_cast<cudaStream_t>(stream_wide)>>>(
         d_insts, n_wide, d_order, d_counter, d_ws, ws, d_counters, pool);
