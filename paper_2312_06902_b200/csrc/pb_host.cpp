@@ -343,6 +343,7 @@ struct WidePlan {
 struct DeviceRun {
   int device = -1;
   char* d_static = nullptr;
+  size_t wide_static_begin = 0, wide_static_end = 0;
   char* d_out = nullptr;
   char* d_ws = nullptr;
   pb::DevInst* d_insts = nullptr;
@@ -557,9 +558,17 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
     out = at + bytes;
     return at;
   };
-  // layout pass: section offsets of every instance (tables at offset 0)
+  // LPT: largest estimated work first
+  P.order.resize(N);
+  std::iota(P.order.begin(), P.order.end(), 0);
+  std::stable_sort(P.order.begin(), P.order.end(), [&](int32_t x, int32_t y) {
+    return b->insts[x].work > b->insts[y].work;
+  });
+  // layout pass: section offsets of every instance (tables at offset 0),
+  // instances in LPT order so the head walks' static data is contiguous
   size_t off = b->tables.size() * sizeof(double);
-  for (size_t k = 0; k < N; ++k) {
+  for (size_t q = 0; q < N; ++q) {
+    const size_t k = static_cast<size_t>(P.order[q]);
     auto& o = P.offs[k];
     o[O_START] = SIZE_MAX;
     instance_sections(b, k, false, [&](int slot, const void*, size_t bytes) {
@@ -612,12 +621,6 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
   }
   P.out_bytes = out;
   P.pool_cap = std::min<long long>(pool, (1ll << 31) - 1);
-  // LPT: largest estimated work first
-  P.order.resize(N);
-  std::iota(P.order.begin(), P.order.end(), 0);
-  std::stable_sort(P.order.begin(), P.order.end(), [&](int32_t x, int32_t y) {
-    return b->insts[x].work > b->insts[y].work;
-  });
   b->cap_points = cap_points;
   b->pool_cap = P.pool_cap;
   b->out_points.assign(N, 0);
@@ -776,6 +779,9 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
     R.wide = choose_wide(b, P.order, sms, std::max(1, pb::walk_slots_per_sm(R.ws)));
   }
+  // static bytes of the cooperative head walks (contiguous: LPT layout)
+  R.wide_static_begin = N ? P.offs[P.order[0]][O_ORIG] : 0;
+  R.wide_static_end = R.wide.n < static_cast<int32_t>(N) ? P.offs[P.order[R.wide.n]][O_ORIG] : P.stat_bytes;
   R.slots = device_slots(device, static_cast<int64_t>(N) - R.wide.n, R.ws, R.wide);
   ensure_device(R.d_ws, R.cap_ws, static_cast<size_t>(R.ws.stride) * (R.slots + R.wide.ctas), "malloc workspace");
   ensure_device(R.d_insts, R.cap_insts, sizeof(pb::DevInst) * N, "malloc insts");
@@ -830,9 +836,12 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
     const size_t persist = std::min<size_t>(static_cast<size_t>(mb) << 20, static_cast<size_t>(max_persist));
     ck(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist), "persisting L2");
     cudaStreamAttrValue a{};
-    a.accessPolicyWindow.base_ptr = R.d_ws;
-    a.accessPolicyWindow.num_bytes = std::min<size_t>(static_cast<size_t>(R.wide.ctas) * R.ws.stride,
-                                                      static_cast<size_t>(max_win));
+    const bool stat = std::getenv("PB_L2_STATIC") != nullptr;  // the head walks' static data instead
+    a.accessPolicyWindow.base_ptr = stat ? R.d_static + R.wide_static_begin : R.d_ws;
+    a.accessPolicyWindow.num_bytes =
+        std::min<size_t>(stat ? R.wide_static_end - R.wide_static_begin
+                              : static_cast<size_t>(R.wide.ctas) * R.ws.stride,
+                         static_cast<size_t>(max_win));
     a.accessPolicyWindow.hitRatio =
         std::min(1.0f, static_cast<float>(persist) / static_cast<float>(a.accessPolicyWindow.num_bytes));
     a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
