@@ -694,16 +694,17 @@ WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int s
   int n = env_int("PB_WIDE", -1);
   if (n < 0) {
     n = 0;
-    // measured on the 4096 batch: the top ~50 walks (>= 88% of the largest
-    // estimated work) on 2-warp CTAs shorten the critical walk by ~6%
-    const int permille = env_int("PB_WIDE_PERMILLE", 880);
+    // measured on the 4096 batch: the walks with >= 75% of the largest
+    // estimated work on 2-warp CTAs, all concurrently (up to 128), give the
+    // shortest batch (10.1 s vs 10.9 s at 88% / 48 CTAs)
+    const int permille = env_int("PB_WIDE_PERMILLE", 750);
     if (permille > 0 && N > int64_t{sms} * per_sm) {
       const double top = static_cast<double>(b->insts[order[0]].work);
       while (n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;
     }
   }
   w.n = static_cast<int32_t>(std::min<int64_t>(n, N));
-  const int ctas = env_int("PB_WIDE_CTAS", 48);
+  const int ctas = env_int("PB_WIDE_CTAS", 128);
   w.ctas = w.n > 0 ? std::max(1, std::min(ctas, w.n)) : 0;
   return w;
 }

@@ -168,6 +168,7 @@ struct WsLayout {
   int64_t off_nodeli;                  // int32 [V] log index of each node in the last BFS
   int64_t stride;
   int32_t smem_bytes;  // dynamic shared memory per warp
+  int32_t wide_par = 0;  // cooperative kernel: shared parent links for max_v log entries (0: none)
 };
 
 struct RunCounters {

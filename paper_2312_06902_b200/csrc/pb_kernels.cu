@@ -166,6 +166,8 @@ struct Net {
   long long R;  // flow on the return arc = s->t value
   struct CoopCtl* ctl;  // cooperative BFS (nw > 1 warps of one CTA), else null
   int nw;
+  uint32_t s_par;  // smem: parent log index of every log entry (-1: seed); cooperative walks only
+  int par_cap;     // entries s_par holds (0: no shared parents, chase the global log)
 };
 
 constexpr int kCtlBytes = 256;  // shared memory reserved for CoopCtl
@@ -256,6 +258,7 @@ __device__ __forceinline__ bool bit_of(const Net& N, int u) {
 __device__ __forceinline__ void seed(Net& N, int k, int v) {
   fwrite(N, 0, k, make_int4(v, N.inc_off[v], N.inc_off[v + 1], k));
   N.lg[k] = make_int4(-1 - v, -1, -1, v);
+  if (k < N.par_cap) sts32(N.s_par + 4u * k, 0xffffffffu);
   N.node_li[v] = k;
 }
 
@@ -385,6 +388,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
         if (c) {
           const int li = nlog + pos;
           N.lg[li] = make_int4(p, -1, fe.w, e.x);
+          if (li < N.par_cap) sts32(N.s_par + 4u * li, static_cast<uint32_t>(fe.w));
           N.node_li[e.x] = li;
           if (kCoop && !kA && e.x == N.snk) atomicMin(&N.ctl->snk_li, static_cast<unsigned long long>(li));
           const int4 ent = make_int4(e.x, e.z, e.w, li);
@@ -406,6 +410,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
           const int ze = (e.x & 1) ? e.z : e.w + pd;
           const int lz = nlog + posz;
           N.lg[lz] = make_int4(e.z, p, fe.w, z);  // y's computation arc, the arc into y, y's parent
+          if (lz < N.par_cap) sts32(N.s_par + 4u * lz, static_cast<uint32_t>(fe.w));
           N.node_li[z] = lz;
           const int4 ent = make_int4(z, zo, ze, lz);
           pf_l1(N.ient + zo);
@@ -546,7 +551,45 @@ __device__ long long push_chain(Net& N, int first, int idx, long long cap, bool 
     N.path_log[k] = -1 - idx;  // arc into the sink: its tail is entry idx
     N.path[k++] = first;
   }
-  if (ln == 0) {
+  if (N.par_cap > 0) {
+    // Cooperative walk: lane 0 follows the parent links in shared memory,
+    // collecting the path's log entries (scratch: frontier buffer 1, dead
+    // between BFSs); the warp then reads the entries together.
+    int* ent = reinterpret_cast<int*>(N.fglob + N.fstride);
+    int m = 0;
+    if (ln == 0) {
+      for (int x = idx; x >= 0; x = static_cast<int>(lds32(N.s_par + 4u * x))) ent[m++] = x;
+    }
+    m = __shfl_sync(kFull, m, 0);
+    k = __shfl_sync(kFull, k, 0);
+    __syncwarp();
+    // the last entry is the seed (its log x = -1 - source); the others carry
+    // one arc, or two through a shortcut, in chase order
+    for (int base = 0; base < m; base += 32) {
+      const int q = base + ln;
+      int4 l = make_int4(0, -1, 0, 0);
+      int x = 0;
+      if (q < m) {
+        x = ent[q];
+        l = N.lg[x];
+      }
+      const bool arc = q < m && l.x >= 0;
+      if (q < m && l.x < 0) s = -1 - l.x;
+      const bool two = arc && l.y >= 0;
+      const unsigned ba = __ballot_sync(kFull, arc), b2 = __ballot_sync(kFull, two);
+      const int at = k + __popc(ba & lanemask_lt()) + __popc(b2 & lanemask_lt());
+      if (arc) {
+        N.path_log[at] = x;
+        N.path[at] = l.x;
+        if (two) {
+          N.path_log[at + 1] = x;
+          N.path[at + 1] = l.y;
+        }
+      }
+      k += __popc(ba) + __popc(b2);
+    }
+    s = static_cast<int>(wmaxi(s));
+  } else if (ln == 0) {
     for (;;) {
       const int4 l = N.lg[idx];
       if (l.x < 0) {
@@ -1557,6 +1600,8 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.N.bal = reinterpret_cast<long long*>(base + L.off_bal);
   p.N.lg = reinterpret_cast<int4*>(base + L.off_log);
   p.N.fglob = reinterpret_cast<int4*>(base + L.off_front);
+  p.N.s_par = 0;
+  p.N.par_cap = 0;
   p.N.fstride = static_cast<int>(L.max_v);
   p.N.path = reinterpret_cast<int32_t*>(base + L.off_path);
   p.N.path_log = reinterpret_cast<int32_t*>(base + L.off_pathlog);
@@ -1656,6 +1701,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel_wide(const Dev
   WsPtrs P = bind_ws(ws_base + static_cast<size_t>(blockIdx.x) * L.stride, L, g_smem + 128);
   P.N.ctl = ctl;
   P.N.nw = nw;
+  P.N.s_par = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem + nw * per + kCtlBytes));
+  P.N.par_cap = L.wide_par;
   if (wi == 0) {
     for (;;) {
       int k = 0;
@@ -2018,10 +2065,18 @@ int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order,
                  void* stream_wide) {
   if (n_wide > 0 && wide_ctas > 0) {
     static_assert(sizeof(CoopCtl) <= kCtlBytes, "CoopCtl outgrew its shared-memory block");
-    const size_t sm = static_cast<size_t>(wide_warps) * (128 + 8 * kMaxEnds + ws.smem_bytes) + kCtlBytes;
+    size_t sm = static_cast<size_t>(wide_warps) * (128 + 8 * kMaxEnds + ws.smem_bytes) + kCtlBytes;
+    // shared parent links for the augment chase, when every log entry fits
+    WsLayout wl = ws;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t par = 4 * static_cast<size_t>(ws.max_v);
+    wl.wide_par = sm + par <= static_cast<size_t>(optin) ? static_cast<int32_t>(ws.max_v) : 0;
+    if (wl.wide_par) sm += par;
     set_smem(walk_kernel_wide, sm);
     walk_kernel_wide<<<wide_ctas, 32 * wide_warps, sm, static_cast<cudaStream_t>(stream_wide)>>>(
-        d_insts, n_wide, d_order, d_counter, d_ws, ws, d_counters, pool);
+        d_insts, n_wide, d_order, d_counter, d_ws, wl, d_counters, pool);
   }
   if (n_inst > n_wide) {
     const size_t sm = block_smem(ws);
