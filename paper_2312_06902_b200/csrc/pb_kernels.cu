@@ -2072,7 +2072,9 @@ int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const size_t par = 4 * static_cast<size_t>(ws.max_v);
-    wl.wide_par = sm + par <= static_cast<size_t>(optin) ? static_cast<int32_t>(ws.max_v) : 0;
+    wl.wide_par = sm + par <= static_cast<size_t>(optin) && !std::getenv("PB_WIDE_NO_SHARED_PARENTS")
+                      ? static_cast<int32_t>(ws.max_v)
+                      : 0;
     if (wl.wide_par) sm += par;
     set_smem(walk_kernel_wide, sm);
     walk_kernel_wide<<<wide_ctas, 32 * wide_warps, sm, static_cast<cudaStream_t>(stream_wide)>>>(

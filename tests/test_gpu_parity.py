@@ -69,11 +69,15 @@ def test_every_golden_walk_in_one_batch(walks):
         check_walk_against(b, k, walks[spec], model.blocking_watts, model.quantum_us, full=spec != "config:2")
 
 
-@pytest.mark.parametrize("warps", [2, 4])
-def test_golden_walks_through_the_cooperative_bfs(walks, monkeypatch, warps):
+@pytest.mark.parametrize("warps,shared_parents", [(2, True), (4, True), (2, False)])
+def test_golden_walks_through_the_cooperative_bfs(walks, monkeypatch, warps, shared_parents):
     """The same 126 walks with every instance on the wide (multi-warp BFS)
-    kernel, and with the wide kernel sharing the batch with the walker."""
+    kernel, and with the wide kernel sharing the batch with the walker; with
+    the augment chase through shared-memory parent links and through the
+    global log (the fallback for instances too large for shared memory)."""
     monkeypatch.setenv("PB_WIDE_WARPS", str(warps))
+    if not shared_parents:
+        monkeypatch.setenv("PB_WIDE_NO_SHARED_PARENTS", "1")
     monkeypatch.setenv("PB_WIDE_CTAS", "7")
     for wide in ("100000", "9"):
         monkeypatch.setenv("PB_WIDE", wide)
