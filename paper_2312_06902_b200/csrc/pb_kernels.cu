@@ -1692,6 +1692,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel_wide(const Dev
                                                            const int32_t* order, int32_t* counter,
                                                            char* ws_base, WsLayout L, RunCounters* ctr,
                                                            DeltaPool pool) {
+  // this CTA is resident: the walker grid (programmatic dependent launch on
+  // the same stream) may start once every cooperative CTA got here, so the
+  // persistent walkers can never take the SMs the cooperative CTAs need
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int nw = blockDim.x >> 5;
   const int wi = warp_in_block();
   Counters C;
@@ -2077,14 +2081,29 @@ int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order,
                       : 0;
     if (wl.wide_par) sm += par;
     set_smem(walk_kernel_wide, sm);
-    walk_kernel_wide<<<wide_ctas, 32 * wide_warps, sm, static_cast<cudaStream_t>(stream_wide)>>>(
+    walk_kernel_wide<<<wide_ctas, 32 * wide_warps, sm, static_cast<cudaStream_t>(stream)>>>(
         d_insts, n_wide, d_order, d_counter, d_ws, wl, d_counters, pool);
   }
+  (void)stream_wide;
   if (n_inst > n_wide) {
     const size_t sm = block_smem(ws);
     set_smem(walk_kernel, sm);
-    walk_kernel<<<blocks_for(slots), kBlock, sm, static_cast<cudaStream_t>(stream)>>>(
-        d_insts, n_inst, d_order, d_counter, d_ws, ws, slots, d_counters, pool, n_wide, wide_ctas);
+    // same stream as the cooperative kernel, programmatic dependent launch:
+    // the walkers start as soon as every cooperative CTA is resident (they
+    // share only the pre-zeroed queue counters, no data)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(blocks_for(slots)));
+    cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = n_wide > 0 && wide_ctas > 0 ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, walk_kernel, d_insts, n_inst, d_order, d_counter, d_ws, ws,
+                                             slots, d_counters, pool, n_wide, wide_ctas);
+    if (e != cudaSuccess) return static_cast<int>(e);
   }
   return static_cast<int>(cudaGetLastError());
 }
