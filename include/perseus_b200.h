@@ -36,7 +36,8 @@ typedef enum {
   PB_ERR_DOMAIN = 4,           /* DegenerateFit, std::domain_error (costmodel.hpp:50-52) */
   PB_ERR_CUDA = 5,             /* device failure (no reference counterpart) */
   PB_ERR_UNSUPPORTED = 6,      /* input outside what the device layout supports
-                                  (e.g. a curve interval too long to tabulate) */
+                                  (a curve interval too long to tabulate, or a
+                                  curve value outside the host tables) */
   PB_ERR_BUDGET = 7            /* BudgetExceeded (oracle.hpp:17-19): assignment
                                   space above the enumeration budget */
 } pb_status;
@@ -104,12 +105,17 @@ typedef struct {
   int32_t stop;   /* pb_stop_reason */
   int32_t status; /* pb_status of this instance */
   int32_t n_ids;  /* total delta records */
-  /* curve evaluations outside [t_min, t_max] (done with device exp instead
-   * of the host table; the reference evaluates the curve there too,
-   * costmodel.hpp:47).  0 on every G9 and golden walk. */
-  int32_t n_extrapolated;
+  /* curve evaluations that fell outside the host-built E_c[t] tables.  The
+   * tables cover every time a walk can evaluate, so
+   * this is 0; if it were not, status is PB_ERR_UNSUPPORTED -- the device
+   * never substitutes its own exp for the reference's libm
+   * (costmodel.hpp:47). */
+  int32_t n_table_misses;
   /* device time of this walk (microseconds, %globaltimer); diagnostics */
   int32_t walk_us;
+  /* warps that walked it: 1 = a walker warp, > 1 = a cooperative CTA */
+  int32_t warps;
+  int32_t pad;
 } pb_frontier_summary;
 
 /* Per-point scalars; point 0 is the T* seed, point k>0 follows step k. */
@@ -162,6 +168,10 @@ pb_status pb_batch_points(const pb_batch* b, int32_t index, pb_point* out, int32
  * -(c + 1) for a slowed-down one; choice[j] = its new Pareto index. */
 pb_status pb_batch_deltas(const pb_batch* b, int32_t index, int32_t* ids, uint8_t* choice,
                           int32_t capacity);
+/* 64-bit digest of instance `index`'s results (summary, point scalars,
+ * delta records in step order; not the device pool offsets): equal digests
+ * across launches = deterministic output. */
+pb_status pb_batch_digest(const pb_batch* b, int32_t index, uint64_t* out);
 /* Materializes schedule k of instance `index` (EnergySchedule fields,
  * frontier.hpp:20-33); any pointer may be NULL.  eff_* are summed in index
  * order exactly as detail::effective_total (frontier.hpp:51-57). */
@@ -277,6 +287,9 @@ pb_status pb_batch_add_g9(pb_batch* b, int32_t stages, int32_t microbatches, int
 /* Config-5 instances [first, first + count) built in parallel on `threads`
  * host threads (0 = all), appended in index order. */
 pb_status pb_batch_add_g9_batch(pb_batch* b, int32_t first, int32_t count, int64_t tau, int32_t threads);
+/* Config-5 instances idx[0..count) (any order, repeats allowed), built in
+ * parallel, appended in list order (an LPT shard of the batch). */
+pb_status pb_batch_add_g9_indices(pb_batch* b, const int32_t* idx, int32_t count, int64_t tau, int32_t threads);
 /* The 9 (freq, time, energy) points of a stage base (descending frequency). */
 pb_status pb_g9_profile(int32_t b, int32_t backward, int64_t tau, int32_t* freq, int64_t* time,
                         int64_t* energy);

@@ -8,6 +8,8 @@
 // Modes
 //   walk <spec>...           frontier walk per instance (discover_frontier
 //                            loop restated with StepInfo, frontier.hpp:166-189)
+//   walkprefix <K> <spec>... the same walk stopped after K steps
+//                            (reason "max_steps" when T_min is not reached)
 //   flow <seed> <count> <max_nodes> <max_cap>
 //                            testutil::random_flow_graph corpus through
 //                            max_flow_lower_bounds + min_cut_from_flow
@@ -20,6 +22,9 @@
 //                            (serde.hpp frontier_csv / schedule_json dump(2))
 //                            for the first, middle and last schedules
 //   brute <spec>...          brute_force_frontier (oracle.hpp:47-114) points
+//   rule5 <first> <count> [maxn]  r5 specs whose walk hits SURVEY §7 rule 5
+//   getnext <tau> (<spec> <t0,t1,...>)...  get_next_schedule from a caller
+//                            schedule (planned times anywhere)
 //   savings <P> <factors,...> <spec>...
 //                            straggler_savings (baselines.hpp:162-188) on the
 //                            reference frontier: rows + the looked-up point
@@ -30,6 +35,7 @@
 //   batch:I                                   config-5 instance I
 //   diamond | lone:ft:fe:st:se                test_frontier.cpp:23-58
 //   grid:seed:stages:micro[:maxpts]           testutil::grid_profiles walk
+//   r5:seed[:maxn]                            random custom DAG (rule-5 search)
 //   cubic:seed:stages:micro                   testutil::cubic_profiles walk
 #include <atomic>
 #include <chrono>
@@ -148,6 +154,30 @@ Instance make_instance(const std::string& spec) {
     }
     in.dag = build_1f1b(stages, micro);
     in.set = testutil::cubic_profiles(stages, {1400, 1300, 1200, 1100, 1000, 900}, 4.0e6, fs, bs);
+  } else if (t[0] == "r5") {
+    // small random custom DAG for the rule-5 search (mode_rule5): every
+    // computation its own class, ~1/3 constant (one Pareto point), the rest
+    // grid profiles with 2-4 points on tau multiples
+    std::mt19937 rng(static_cast<std::uint32_t>(std::stoul(t[1])));
+    const int n = std::uniform_int_distribution<int>(3, t.size() > 2 ? std::stoi(t[2]) : 8)(rng);
+    std::vector<Computation> comps;
+    for (int i = 0; i < n; ++i) comps.push_back(Computation{i, i, 0, Kind::Forward});
+    std::vector<std::pair<int, int>> edges;
+    std::uniform_real_distribution<double> coin(0, 1);
+    for (int u = 0; u < n; ++u)
+      for (int v = u + 1; v < n; ++v)
+        if (coin(rng) < 0.4) edges.emplace_back(u, v);
+    in.dag = finalize_custom_dag(comps, edges);
+    in.set.p_blocking_watts = kDefaultBlockingWatts;
+    for (int i = 0; i < n; ++i) {
+      if (coin(rng) < 0.35) {
+        const Quanta b = std::uniform_int_distribution<int>(1, 9)(rng) * 1000;
+        in.set.profiles.push_back(  // dominated slow point: Pareto set collapses to one point
+            {ClassKey{i, Kind::Forward}, {ProfilePoint{1400, b, 3000}, ProfilePoint{1200, b + 1000, 3500}}});
+      } else {
+        in.set.profiles.push_back(testutil::grid_profile(rng, ClassKey{i, Kind::Forward}, 1000, 4, false));
+      }
+    }
   } else {
     std::fprintf(stderr, "unknown spec %s\n", spec.c_str());
     std::exit(2);
@@ -263,7 +293,7 @@ std::string curves_json(const CostModel& m) {
 // discover_frontier (frontier.hpp:166-189) restated step by step so that
 // StepInfo and the terminal reason are observable; cross-checked against
 // discover_frontier itself for small instances (check=true).
-std::string walk_json(const Instance& in, bool full, bool check) {
+std::string walk_json(const Instance& in, bool full, bool check, long long max_steps = -1) {
   const auto t0 = std::chrono::steady_clock::now();
   const AllMaxAssignment am = all_max_assignment(in.dag, in.model);
   const Quanta t_min = simulate(in.dag, am.durations).iteration_time;
@@ -275,6 +305,10 @@ std::string walk_json(const Instance& in, bool full, bool check) {
   std::vector<Quanta> step_sizes;
   std::string reason = "at_t_min";
   while (cur.t_planned > t_min) {
+    if (max_steps >= 0 && static_cast<long long>(infos.size()) >= max_steps) {
+      reason = "max_steps";
+      break;
+    }
     const Quanta step = std::min<Quanta>(in.tau, cur.t_planned - t_min);
     StepInfo info;
     auto next = get_next_schedule(in.dag, cur, in.model, step, &info);
@@ -630,6 +664,84 @@ int mode_budget(int argc, char** argv) {
   return 0;
 }
 
+// get_next_schedule (frontier.hpp:90-135) from a caller schedule: planned
+// times given (comma-separated, any value -- also outside a class's curve
+// interval), planned energies from detail::planned_energy.
+int mode_getnext(int argc, char** argv) {
+  const Quanta tau = std::stoll(argv[2]);
+  for (int i = 3; i + 1 < argc; i += 2) {
+    const Instance in = make_instance(argv[i]);
+    EnergySchedule s;
+    for (const auto& tok : split(argv[i + 1], ',')) s.planned_t.push_back(std::stoll(tok));
+    for (size_t c = 0; c < s.planned_t.size(); ++c)
+      s.planned_e.push_back(
+          detail::planned_energy(in.model.require(class_of(in.dag.computations[c])), s.planned_t[c]));
+    detail::refresh_totals(in.dag, in.model, s);
+    std::string o = "{\"spec\":\"" + std::string(argv[i]) + "\",\"tau\":" + std::to_string(tau) +
+                    ",\"start\":";
+    put_list(o, s.planned_t);
+    o += ",\"start_e\":";
+    put_list(o, s.planned_e);
+    StepInfo info;
+    const auto nx = get_next_schedule(in.dag, s, in.model, tau, &info);
+    if (!nx) {
+      o += ",\"next\":null}";
+    } else {
+      o += ",\"cut_cost\":" + std::to_string(info.cut_cost) + ",\"sped\":";
+      put_list(o, info.sped_up);
+      o += ",\"slowed\":";
+      put_list(o, info.slowed_down);
+      o += ",\"planned_t\":";
+      put_list(o, nx->planned_t);
+      o += ",\"planned_e\":";
+      put_list(o, nx->planned_e);
+      o += ",\"t_planned\":" + std::to_string(nx->t_planned) + ",\"eff_planned\":" + dbl(nx->eff_planned_mj) + "}";
+    }
+    std::printf("%s\n", o.c_str());
+  }
+  (void)argc;
+  return 0;
+}
+
+// Rule-5 search (SURVEY.md §7 parity rule 5): walks r5:<seed> instances and
+// reports the specs whose walk speeds up a computation through an infinite
+// edge inside a cut of value < sentinel (a constant class, or a planned time
+// pushed below the curve's t_min: frontier.hpp:111-116 has no bound check).
+int mode_rule5(int argc, char** argv) {
+  const std::uint32_t first = static_cast<std::uint32_t>(std::stoul(argv[2]));
+  const int count = std::stoi(argv[3]);
+  const std::string maxn = argc > 4 ? argv[4] : "8";
+  for (int q = 0; q < count; ++q) {
+    const std::string spec = "r5:" + std::to_string(first + q) + ":" + maxn;
+    const Instance in = make_instance(spec);
+    const AllMaxAssignment am = all_max_assignment(in.dag, in.model);
+    const Quanta t_min = simulate(in.dag, am.durations).iteration_time;
+    EnergySchedule cur = min_energy_schedule(in.dag, in.model);
+    int steps = 0, events = 0, below = 0, first_step = -1;
+    while (cur.t_planned > t_min && steps < 2000) {
+      const Quanta step = std::min<Quanta>(in.tau, cur.t_planned - t_min);
+      StepInfo info;
+      auto next = get_next_schedule(in.dag, cur, in.model, step, &info);
+      if (!next || next->t_planned >= cur.t_planned) break;
+      for (int c : info.sped_up) {
+        const auto& cm = in.model.require(class_of(in.dag.computations[c]));
+        const bool ev = cm.is_constant || next->planned_t[c] < cm.curve->t_min;
+        if (ev) {
+          ++events;
+          if (!cm.is_constant && next->planned_t[c] < cm.curve->t_min - in.tau) ++below;
+          if (first_step < 0) first_step = steps;
+        }
+      }
+      cur = std::move(*next);
+      ++steps;
+    }
+    if (events)
+      std::printf("{\"spec\":\"%s\",\"steps\":%d,\"events\":%d,\"below_tau\":%d,\"first\":%d}\n",
+                  spec.c_str(), steps, events, below, first_step);
+  }
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -647,6 +759,17 @@ int main(int argc, char** argv) {
       }
       return 0;
     }
+    if (mode == "walkprefix") {  // walkprefix <max_steps> <spec>...: the first K steps only
+      const long long k = std::stoll(argv[2]);
+      for (int i = 3; i < argc; ++i) {
+        const Instance in = make_instance(argv[i]);
+        std::printf("%s\n", walk_json(in, false, false, k).c_str());
+        std::fflush(stdout);
+      }
+      return 0;
+    }
+    if (mode == "rule5") return mode_rule5(argc, argv);
+    if (mode == "getnext") return mode_getnext(argc, argv);
     if (mode == "flow") return mode_flow(argc, argv);
     if (mode == "slack") return mode_slack(argc, argv);
     if (mode == "bench") return mode_bench(argc, argv);

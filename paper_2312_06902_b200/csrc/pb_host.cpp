@@ -360,8 +360,8 @@ struct DeviceRun {
   // allocated capacities (buffers are reused across runs while they fit)
   size_t cap_static = 0, cap_out = 0, cap_ws = 0, cap_insts = 0, cap_order = 0;
   long long cap_pool = 0;
-  cudaStream_t stream = nullptr, stream_big = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_big = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   WidePlan wide;
   char* h_out = nullptr;  // pinned
   void release() {
@@ -380,9 +380,7 @@ struct DeviceRun {
     if (h_out) cudaFreeHost(h_out);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (ev_big) cudaEventDestroy(ev_big);
     if (stream) cudaStreamDestroy(stream);
-    if (stream_big) cudaStreamDestroy(stream_big);
     *this = DeviceRun{};
   }
 };
@@ -393,7 +391,8 @@ struct pb_batch {
   std::vector<HostInst> insts;
   // packed host-side view (tables kept for host expansion)
   std::vector<double> tables;
-  std::vector<std::vector<int64_t>> cls_tab;  // per instance per class
+  std::vector<std::vector<int64_t>> cls_tab;  // per instance per class: table offset of E(t_min)
+  std::vector<std::pair<int64_t, int64_t>> tab_margin;  // per instance: table extent below t_min / above t_max
   // outputs (host copies)
   std::vector<size_t> out_points, out_summary;
   std::vector<int32_t> cap_points;
@@ -522,6 +521,26 @@ void instance_sections(const pb_batch* b, size_t k, bool fill, F&& f) {
 void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_scale) {
   const size_t N = b->insts.size();
   // curve tables, deduplicated by (a, b, c, t_min, t_max) bit patterns
+  // A discover walk only evaluates curves inside [t_min, t_max]: speed-ups
+  // cross finite S->T edges (can_speed: t - tau >= t_min) and slow-downs are
+  // bounded by t_max (frontier.hpp:117-125).  The cut of a feasible network
+  // never holds an infinite S->T edge below the sentinel ("Rule
+  // 5"), so frontier.hpp:111-116's unchecked speed-up cannot leave the range
+  // either.  A get-next start schedule may lie anywhere: its tables are
+  // widened to cover every start time +- tau.
+  b->tab_margin.assign(N, {0, 0});
+  for (size_t k = 0; k < N; ++k) {
+    const HostInst& h = b->insts[k];
+    if (h.start.empty()) continue;
+    int64_t mlo = 0, mhi = 0;
+    for (int32_t i = 0; i < h.n; ++i) {
+      const int32_t c = h.comp_class[i];
+      if (h.cls_const[c]) continue;
+      mlo = std::max(mlo, h.cls_trange[2 * c] - (h.start[i] - h.tau));
+      mhi = std::max(mhi, h.start[i] + h.tau - h.cls_trange[2 * c + 1]);
+    }
+    b->tab_margin[k] = {mlo, mhi};
+  }
   std::map<CurveKey, int64_t> table_of;
   b->tables.clear();
   b->cls_tab.assign(N, {});
@@ -533,19 +552,20 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
       if (h.cls_const[c]) continue;
       const double a = h.cls_curve[3 * c], bb = h.cls_curve[3 * c + 1], cc = h.cls_curve[3 * c + 2];
       const int64_t lo = h.cls_trange[2 * c], hi = h.cls_trange[2 * c + 1];
-      const CurveKey key{bits(a), bits(bb), bits(cc), lo, hi};
+      const int64_t tlo = lo - b->tab_margin[k].first, thi = hi + b->tab_margin[k].second;
+      const CurveKey key{bits(a), bits(bb), bits(cc), tlo, thi};
       auto it = table_of.find(key);
       if (it == table_of.end()) {
         const int64_t at = static_cast<int64_t>(b->tables.size());
-        const int64_t span = hi - lo + 1;
+        const int64_t span = thi - tlo + 1;
         if (span > (int64_t{1} << 27)) throw std::length_error("curve interval too long to tabulate");
         b->tables.resize(b->tables.size() + span);
         // ExpCurve::eval (costmodel.hpp:47), same expression and libm
-        for (int64_t t = lo; t <= hi; ++t)
-          b->tables[at + (t - lo)] = a * std::exp(bb * static_cast<double>(t)) + cc;
+        for (int64_t t = tlo; t <= thi; ++t)
+          b->tables[at + (t - tlo)] = a * std::exp(bb * static_cast<double>(t)) + cc;
         it = table_of.emplace(key, at).first;
       }
-      b->cls_tab[k][c] = it->second;
+      b->cls_tab[k][c] = it->second + (lo - tlo);  // offset of E(t_min)
     }
   }
   P.dev.assign(N, pb::DevInst{});
@@ -613,6 +633,8 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
     d.max_steps = h.start.empty() ? h.max_steps : (h.max_steps == 0 ? 1 : h.max_steps);
     d.cap_points = cap_points[k];
     d.tau = h.tau;
+    d.tab_mlo = b->tab_margin[k].first;
+    d.tab_mhi = b->tab_margin[k].second;
     d.watts = h.watts;
     d.quantum = h.quantum;
     P.max_n = std::max<int64_t>(P.max_n, d.n);
@@ -720,6 +742,21 @@ int32_t device_slots(int device, int64_t n_walk, const pb::WsLayout& ws, const W
       std::max<int64_t>(std::min<int64_t>(n_walk, int64_t{sms} * per_sm - wide_warps), std::min<int64_t>(n_walk, 4)));
 }
 
+// Device allocation owned by one call: freed on every exit path, including
+// the CudaError thrown by a later ck().
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  DevBuf(size_t count, const char* what) {
+    ck(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * std::max<size_t>(count, 1)), what);
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
 // (Re)allocates a device buffer only when the current one is too small.
 template <class T>
 void ensure_device(T*& ptr, size_t& cap, size_t bytes, const char* what) {
@@ -745,8 +782,6 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   if (R.device < 0) {
     R.device = device;
     ck(cudaStreamCreateWithFlags(&R.stream, cudaStreamNonBlocking), "stream");
-    ck(cudaStreamCreateWithFlags(&R.stream_big, cudaStreamNonBlocking), "stream");
-    ck(cudaEventCreateWithFlags(&R.ev_big, cudaEventDisableTiming), "event");
     ck(cudaEventCreate(&R.ev0), "event");
     ck(cudaEventCreate(&R.ev1), "event");
     ck(cudaMalloc(&R.d_counter, 2 * sizeof(int32_t)), "malloc counter");
@@ -847,19 +882,16 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
         std::min(1.0f, static_cast<float>(persist) / static_cast<float>(a.accessPolicyWindow.num_bytes));
     a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    ck(cudaStreamSetAttribute(R.stream_big, cudaStreamAttributeAccessPolicyWindow, &a), "L2 window");
+    ck(cudaStreamSetAttribute(R.stream, cudaStreamAttributeAccessPolicyWindow, &a), "L2 window");
     if (std::getenv("PB_L2_VERBOSE"))
       std::fprintf(stderr, "L2 persist %zu of max %d, window %zu (max %d), hit %.2f\n", persist, max_persist,
                    a.accessPolicyWindow.num_bytes, max_win, a.accessPolicyWindow.hitRatio);
   }
   ck(cudaEventRecord(R.ev0, R.stream), "record");
-  ck(cudaStreamWaitEvent(R.stream_big, R.ev0, 0), "wait");
   const int rc = pb::launch_walks(R.d_insts, static_cast<int32_t>(N), R.d_order, R.d_counter,
                                   R.d_ws, R.ws, R.slots, R.d_counters, pool, R.wide.n, R.wide.ctas,
-                                  R.wide.warps, R.stream, R.stream_big);
+                                  R.wide.warps, R.stream);
   if (rc != 0) throw CudaError(std::string("walk launch: ") + cudaGetErrorString(static_cast<cudaError_t>(rc)));
-  ck(cudaEventRecord(R.ev_big, R.stream_big), "record");
-  ck(cudaStreamWaitEvent(R.stream, R.ev_big, 0), "wait");
   ck(cudaEventRecord(R.ev1, R.stream), "record");
   ck(cudaStreamSynchronize(R.stream), "walk kernel");
   float ms = 0;
@@ -1127,14 +1159,18 @@ pb_status pb_batch_run_multi(pb_batch* b, int32_t n_devices, const int32_t* devi
     }
     std::vector<pb_batch> subs(n_devices);
     std::vector<pb_status> st(n_devices, PB_OK);
+    std::vector<std::string> msg(n_devices);  // g_last_error is thread_local: carry it back
     std::vector<std::thread> th;
     for (int d = 0; d < n_devices; ++d) {
       for (size_t k : part[d]) subs[d].insts.push_back(b->insts[k]);
-      th.emplace_back([&, d] { st[d] = pb_batch_run(&subs[d], devices[d]); });
+      th.emplace_back([&, d] {
+        st[d] = pb_batch_run(&subs[d], devices[d]);
+        if (st[d] != PB_OK) msg[d] = g_last_error;
+      });
     }
     for (auto& t : th) t.join();
     for (int d = 0; d < n_devices; ++d)
-      if (st[d] != PB_OK) return st[d];
+      if (st[d] != PB_OK) return fail(st[d], "device " + std::to_string(devices[d]) + ": " + msg[d]);
     // stitch results back in the original order
     b->run.release();
     std::vector<char> out;
@@ -1149,9 +1185,12 @@ pb_status pb_batch_run_multi(pb_batch* b, int32_t n_devices, const int32_t* devi
     b->stats = pb_run_stats{};
     for (int d = 0; d < n_devices; ++d) {
       const pb_batch& s = subs[d];
-      const size_t base = out.size();
+      // the sub-batch's results live in its pinned buffer (fetch_impl), valid
+      // while `subs` is alive: copy them, keeping 256 B alignment
+      const size_t base = (out.size() + 255) / 256 * 256;
       const long long pbase = static_cast<long long>(b->pool_ids.size());
-      out.insert(out.end(), s.out.begin(), s.out.end());
+      out.resize(base);
+      if (!s.insts.empty()) out.insert(out.end(), s.outp, s.outp + s.run.out_bytes);
       b->pool_ids.insert(b->pool_ids.end(), s.pool_ids.begin(), s.pool_ids.end());
       b->pool_choice.insert(b->pool_choice.end(), s.pool_choice.begin(), s.pool_choice.end());
       const int64_t tbase = static_cast<int64_t>(b->tables.size());
@@ -1221,6 +1260,38 @@ pb_status pb_batch_deltas(const pb_batch* b, int32_t k, int32_t* ids, uint8_t* c
       if (choice) choice[j] = b->pool_choice[at + r];
     }
   }
+  return PB_OK;
+}
+
+// 64-bit digest of one walk's outputs: summary, every point's scalars (not
+// the device pool offsets, which depend on the order of concurrent
+// reservations) and the delta records in step order.
+pb_status pb_batch_digest(const pb_batch* b, int32_t k, uint64_t* out) {
+  pb_frontier_summary s;
+  const pb_status st = pb_batch_summary(b, k, &s);
+  if (st != PB_OK) return st;
+  if (!out) return fail(PB_ERR_INVALID_ARGUMENT, "null argument");
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    h ^= v;
+    h *= 1099511628211ull;
+    h ^= h >> 29;
+  };
+  for (int64_t v : {s.t_min, s.t_star, int64_t{s.steps}, int64_t{s.stop}, int64_t{s.status}, int64_t{s.n_ids}})
+    mix(static_cast<uint64_t>(v));
+  const pb_point* pts = reinterpret_cast<const pb_point*>(b->outp + b->out_points[k]);
+  const int32_t np = s.status == PB_OK ? s.steps + 1 : 0;
+  for (int32_t q = 0; q < np; ++q) {
+    const pb_point& p = pts[q];
+    for (int64_t v : {p.t_planned, p.t_realized, p.sum_planned_e, p.sum_planned_t, p.sum_realized_e,
+                      p.sum_realized_t, p.cut_cost, p.step_size, int64_t{p.n_sped}, int64_t{p.n_slowed}})
+      mix(static_cast<uint64_t>(v));
+    if (q == 0) continue;
+    const long long at = b->pool_base[k] + p.id_begin;
+    for (int32_t r = 0; r < p.n_sped + p.n_slowed; ++r)
+      mix((static_cast<uint64_t>(static_cast<uint32_t>(b->pool_ids[at + r])) << 8) | b->pool_choice[at + r]);
+  }
+  *out = h;
   return PB_OK;
 }
 
@@ -1474,22 +1545,16 @@ pb_status pb_batch_straggler(pb_batch* b, int32_t n_factors, const double* facto
       J.pad = 0;
       if (num_stages[k] < 1) return fail(PB_ERR_INVALID_ARGUMENT, "num_stages must be positive");
     }
-    pb::DevStraggler* d_jobs = nullptr;
-    double* d_f = nullptr;
-    pb_savings_row* d_out = nullptr;
     const size_t rows = static_cast<size_t>(N) * n_factors;
-    ck(cudaMalloc(&d_jobs, sizeof(pb::DevStraggler) * N), "malloc");
-    ck(cudaMalloc(&d_f, sizeof(double) * n_factors), "malloc");
-    ck(cudaMalloc(&d_out, sizeof(pb_savings_row) * rows), "malloc");
-    ck(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(pb::DevStraggler) * N, cudaMemcpyHostToDevice, R.stream), "H2D");
-    ck(cudaMemcpyAsync(d_f, factors, sizeof(double) * n_factors, cudaMemcpyHostToDevice, R.stream), "H2D");
-    const int rc = pb::launch_straggler(d_jobs, N, d_f, n_factors, pipelines, d_out, R.stream);
+    DevBuf<pb::DevStraggler> d_jobs(N, "malloc straggler jobs");
+    DevBuf<double> d_f(n_factors, "malloc factors");
+    DevBuf<pb_savings_row> d_out(rows, "malloc savings rows");
+    ck(cudaMemcpyAsync(d_jobs.p, jobs.data(), sizeof(pb::DevStraggler) * N, cudaMemcpyHostToDevice, R.stream), "H2D");
+    ck(cudaMemcpyAsync(d_f.p, factors, sizeof(double) * n_factors, cudaMemcpyHostToDevice, R.stream), "H2D");
+    const int rc = pb::launch_straggler(d_jobs.p, N, d_f.p, n_factors, pipelines, d_out.p, R.stream);
     if (rc) throw CudaError(cudaGetErrorString(static_cast<cudaError_t>(rc)));
-    ck(cudaMemcpyAsync(out, d_out, sizeof(pb_savings_row) * rows, cudaMemcpyDeviceToHost, R.stream), "D2H");
+    ck(cudaMemcpyAsync(out, d_out.p, sizeof(pb_savings_row) * rows, cudaMemcpyDeviceToHost, R.stream), "D2H");
     ck(cudaStreamSynchronize(R.stream), "straggler kernel");
-    cudaFree(d_jobs);
-    cudaFree(d_f);
-    cudaFree(d_out);
     return PB_OK;
   });
 }
@@ -1967,11 +2032,13 @@ pb_status pb_batch_add_g9(pb_batch* b, int32_t stages, int32_t microbatches, int
   return pb_batch_add(b, &d, out_index);
 }
 
-// Config-5 instances [first, first + count) built on all host threads
-// (batched CostModel::build + DAG derivation), appended
-// in index order.
-pb_status pb_batch_add_g9_batch(pb_batch* b, int32_t first, int32_t count, int64_t tau, int32_t threads) {
-  if (!b || first < 0 || count < 0) return fail(PB_ERR_INVALID_ARGUMENT, "bad argument");
+// Config-5 instances idx[0..count) built on all host threads (batched
+// CostModel::build + DAG derivation), appended in list
+// order.
+pb_status pb_batch_add_g9_indices(pb_batch* b, const int32_t* idx, int32_t count, int64_t tau, int32_t threads) {
+  if (!b || count < 0 || (count > 0 && !idx)) return fail(PB_ERR_INVALID_ARGUMENT, "bad argument");
+  for (int32_t q = 0; q < count; ++q)
+    if (idx[q] < 0) return fail(PB_ERR_INVALID_ARGUMENT, "negative instance index");
   if (count == 0) return PB_OK;
   const int32_t nt = std::max(1, std::min<int32_t>(threads > 0 ? threads : static_cast<int32_t>(std::thread::hardware_concurrency()), count));
   std::vector<pb_batch> parts(nt);
@@ -1981,10 +2048,10 @@ pb_status pb_batch_add_g9_batch(pb_batch* b, int32_t first, int32_t count, int64
   const int32_t chunk = (count + nt - 1) / nt;
   for (int32_t t = 0; t < nt; ++t)
     pool.emplace_back([&, t] {
-      for (int32_t i = first + t * chunk; i < std::min(first + count, first + (t + 1) * chunk); ++i) {
-        const pb_g9::Params q = pb_g9::batch_instance(i);
-        st[t] = pb_batch_add_g9(&parts[t], q.stages, q.microbatches, q.base, q.imbalance, q.seed, q.straggler_stage,
-                                q.phi, tau, nullptr);
+      for (int32_t q = t * chunk; q < std::min(count, (t + 1) * chunk); ++q) {
+        const pb_g9::Params p = pb_g9::batch_instance(idx[q]);
+        st[t] = pb_batch_add_g9(&parts[t], p.stages, p.microbatches, p.base, p.imbalance, p.seed, p.straggler_stage,
+                                p.phi, tau, nullptr);
         if (st[t] != PB_OK) {
           err[t] = g_last_error;
           return;
@@ -1998,6 +2065,13 @@ pb_status pb_batch_add_g9_batch(pb_batch* b, int32_t first, int32_t count, int64
     for (auto& h : part.insts) b->insts.push_back(std::move(h));
   b->have_results = false;
   return PB_OK;
+}
+
+pb_status pb_batch_add_g9_batch(pb_batch* b, int32_t first, int32_t count, int64_t tau, int32_t threads) {
+  if (!b || first < 0 || count < 0) return fail(PB_ERR_INVALID_ARGUMENT, "bad argument");
+  std::vector<int32_t> idx(count);
+  std::iota(idx.begin(), idx.end(), first);
+  return pb_batch_add_g9_indices(b, idx.data(), count, tau, threads);
 }
 
 pb_status pb_g9_profile(int32_t b, int32_t backward, int64_t tau, int32_t* freq, int64_t* time,

@@ -86,6 +86,10 @@ struct DevInst {
   int64_t tau;
   double watts;
   int64_t quantum;
+  // curve tables cover [t_min - tab_mlo, t_max + tab_mhi] per class (0, 0 for
+  // a discover walk, whose planned times never leave [t_min, t_max]; a
+  // get-next start schedule widens them, pack())
+  int64_t tab_mlo, tab_mhi;
   // node DAG (internal ids)
   const int32_t* orig;        // [n]
   const int32_t* comp_class;  // [n]
@@ -114,8 +118,8 @@ struct DevInst {
   const int32_t* cls_pt_off;  // [classes + 1]
   const int64_t* pt_time;
   const int64_t* pt_energy;
-  const double* tables;           // E(t) = a exp(b t) + c for t in [t_min, t_max]
-  const double* cls_curve;        // [3 * classes] a, b, c (extrapolation only)
+  const double* tables;           // E(t) = a exp(b t) + c for t in [t_min - tab_mlo, t_max + tab_mhi]
+  const double* cls_curve;        // [3 * classes] a, b, c (host expansion only)
   const int64_t* start_planned_t; // get-next mode only (internal order)
   // outputs; delta records go to the batch-wide pool (DeltaPool)
   pb_point* points;             // [cap_points]
@@ -294,8 +298,7 @@ int launch_brute(const DevBrute* d_job, const DevBrute& host_job, int pass, void
 // Workspace slots: [0, wide_ctas) wide CTAs, [wide_ctas, +slots) walkers.
 int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
                  char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
-                 DeltaPool pool, int32_t n_wide, int32_t wide_ctas, int32_t wide_warps, void* stream,
-                 void* stream_wide);
+                 DeltaPool pool, int32_t n_wide, int32_t wide_ctas, int32_t wide_warps, void* stream);
 int walk_slots_per_sm(const WsLayout& ws);
 int launch_flow_jobs(const DevFlowJob* d_jobs, int32_t count, char* d_ws, const WsLayout& ws,
                      int32_t slots, void* stream);

@@ -1000,13 +1000,16 @@ __device__ __forceinline__ int discretize_choice(const DevInst& I, int c, long l
 }
 
 // ExpCurve::eval (costmodel.hpp:47) from the host table (bit-identical to the
-// reference's libm values); outside [t_min, t_max] -- reachable only from a
-// caller-supplied start schedule or the infinite-edge cut case (SURVEY.md §7
-// parity rule 5) -- the device evaluates the curve itself and counts it.
-__device__ __forceinline__ double table_at(const DevInst& I, int c, long long t, int* extrap) {
-  if (t >= I.cls_tmin[c] && t <= I.cls_tmax[c]) return I.tables[I.cls_tab[c] + (t - I.cls_tmin[c])];
-  ++*extrap;
-  return I.cls_curve[3 * c] * exp(I.cls_curve[3 * c + 1] * static_cast<double>(t)) + I.cls_curve[3 * c + 2];
+// reference's libm values).  The table covers every time a walk can evaluate
+// (pack(): [t_min, t_max] for a discover walk, widened around a get-next
+// start schedule), so a miss cannot happen; if it ever did, the miss is
+// counted and the walk ends with PB_ERR_UNSUPPORTED -- the device never
+// substitutes its own exp for glibc's.
+__device__ __forceinline__ double table_at(const DevInst& I, int c, long long t, int* miss) {
+  const long long t0 = I.cls_tmin[c];
+  if (t >= t0 - I.tab_mlo && t <= I.cls_tmax[c] + I.tab_mhi) return I.tables[I.cls_tab[c] + (t - t0)];
+  ++*miss;
+  return 0.0;
 }
 
 // planned_energy (frontier.hpp:59-62).
@@ -1037,12 +1040,11 @@ __device__ void write_point(const DevInst& I, int k, long long tp, long long tr,
 __device__ __forceinline__ int ec_tail_of(int n, int u) { return u == n ? 2 * n : 2 * u + 1; }
 __device__ __forceinline__ int ec_head_of(int n, int v) { return v == n + 1 ? 2 * n + 1 : 2 * v; }
 
-// Curve value at t for a computation record: the host table inside
-// [t_min, t_max], the curve itself outside (counted, SURVEY.md §7 rule 5).
-__device__ __forceinline__ double table_rec(const DevInst& I, const CompRec& rc, int i, long long t,
-                                            int* extrap) {
-  if (t >= rc.tmin && t <= rc.tmax) return I.tables[rc.tab + (t - rc.tmin)];
-  return table_at(I, I.comp_class[i], t, extrap);
+// Curve value at t for a computation record (table_at).
+__device__ __forceinline__ double table_rec(const DevInst& I, const CompRec& rc, long long t, int* miss) {
+  if (t >= rc.tmin - I.tab_mlo && t <= rc.tmax + I.tab_mhi) return I.tables[rc.tab + (t - rc.tmin)];
+  ++*miss;
+  return 0.0;
 }
 
 // Totals of the critical network (flow.hpp:58-68, 196-197), maintained
@@ -1226,13 +1228,13 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
       if (crit && rc.tab >= 0) {
         const bool can_speed = t - step >= rc.tmin;
         const bool can_slow = t + step <= rc.tmax;
-        const double et = (can_speed || can_slow) ? table_rec(I, rc, i, t, extrap) : 0.0;
+        const double et = (can_speed || can_slow) ? table_rec(I, rc, t, extrap) : 0.0;
         if (can_slow) {
-          const long long r = llround(et - table_rec(I, rc, i, t + step, extrap));
+          const long long r = llround(et - table_rec(I, rc, t + step, extrap));
           l = r > 0 ? r : 0;
         }
         if (can_speed) {
-          const long long r = llround(table_rec(I, rc, i, t - step, extrap) - et);
+          const long long r = llround(table_rec(I, rc, t - step, extrap) - et);
           u = r > l ? r : l;
           inf = false;
         }
@@ -1409,12 +1411,13 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   if (ln == 0) write_point(I, 0, t_cur, t_real, spe, spt, sre, srt, 0, 0, 0, 0, 0);
   int steps = 0;
   long long n_ids = 0;
-  int status = PB_OK;
+  // a curve evaluation outside the host tables ends the walk (table_at)
+  int status = __any_sync(kFull, bad != 0) ? PB_ERR_UNSUPPORTED : PB_OK;
   int stop = PB_STOP_AT_TMIN;
   long long prev_step = -1;
   CapSums sums{0, 0, 0};
 
-  for (;;) {
+  while (status == PB_OK) {
     long long step;
     if (I.mode == kModeDiscover) {
       if (!(t_cur > t_min)) {
@@ -1439,8 +1442,8 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     prev_step = step;
     int jprev = -1;
     const int cs = build_caps(I, N, W, step, step_changed, t_cur, sums, ntouch, &bad, C, jprev);
-    if (cs != PB_OK) {
-      status = cs;
+    if (cs != PB_OK || __any_sync(kFull, bad != 0)) {
+      status = cs != PB_OK ? cs : PB_ERR_UNSUPPORTED;
       break;
     }
     // ---- K4 warm-started max flow with lower bounds
@@ -1544,7 +1547,10 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     }
     imin = __reduce_min_sync(kFull, imin);
     imax = __reduce_max_sync(kFull, imax);
-    __syncwarp();
+    if (__any_sync(kFull, bad != 0)) {
+      status = PB_ERR_UNSUPPORTED;
+      break;
+    }
     const int ns = static_cast<int>(wsum(ns_loc));
     dpe = wsum(dpe);
     dpt = wsum(dpt);
@@ -1572,7 +1578,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     n_ids += nd;
   }
   __syncwarp();
-  const long long n_extrap = wsum(bad);
+  const long long n_miss = wsum(bad);
   C.add(kPrWalk, now() - t_walk0);
   if (ln == 0) {
     pb_frontier_summary s;
@@ -1582,8 +1588,10 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     s.stop = stop;
     s.status = status;
     s.n_ids = static_cast<int32_t>(n_ids);
-    s.n_extrapolated = static_cast<int32_t>(n_extrap);
+    s.n_table_misses = static_cast<int32_t>(n_miss);
     s.walk_us = static_cast<int32_t>((gtimer() - g0) / 1000);
+    s.warps = N.nw;
+    s.pad = 0;
     *I.summary = s;
   }
   __syncwarp();
@@ -2065,8 +2073,7 @@ int walk_slots_per_sm(const WsLayout& ws) {
 // d_counter[0] = walker queue cursor, d_counter[1] = wide queue cursor.
 int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
                  char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
-                 DeltaPool pool, int32_t n_wide, int32_t wide_ctas, int32_t wide_warps, void* stream,
-                 void* stream_wide) {
+                 DeltaPool pool, int32_t n_wide, int32_t wide_ctas, int32_t wide_warps, void* stream) {
   if (n_wide > 0 && wide_ctas > 0) {
     static_assert(sizeof(CoopCtl) <= kCtlBytes, "CoopCtl outgrew its shared-memory block");
     size_t sm = static_cast<size_t>(wide_warps) * (128 + 8 * kMaxEnds + ws.smem_bytes) + kCtlBytes;
@@ -2084,7 +2091,6 @@ int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order,
     walk_kernel_wide<<<wide_ctas, 32 * wide_warps, sm, static_cast<cudaStream_t>(stream)>>>(
         d_insts, n_wide, d_order, d_counter, d_ws, wl, d_counters, pool);
   }
-  (void)stream_wide;
   if (n_inst > n_wide) {
     const size_t sm = block_smem(ws);
     set_smem(walk_kernel, sm);

@@ -151,6 +151,21 @@ class FrontierBatch:
             p = g9.batch_params(i)
             self._packed.append(_G9Meta(2 * p.stages * p.microbatches))
 
+    def add_g9_indices(self, indices, tau: int = 1000, threads: int = 0) -> None:
+        """Config-5 instances ``indices`` (e.g. an LPT shard), built on all host threads."""
+        from . import g9
+        idx = np.ascontiguousarray(list(indices), np.int32)
+        N.check(N.lib.pb_batch_add_g9_indices(self._h, N.ptr(idx, C.c_int32), len(idx), tau, threads))
+        for i in idx.tolist():
+            p = g9.batch_params(i)
+            self._packed.append(_G9Meta(2 * p.stages * p.microbatches))
+
+    def digest(self, k: int) -> int:
+        """64-bit digest of instance k's results (pb_batch_digest)."""
+        d = C.c_uint64()
+        N.check(N.lib.pb_batch_digest(self._h, k, C.byref(d)))
+        return d.value
+
     def brute_force(self, k: int, budget: float = 1e7, device: int = 0):
         """brute_force_frontier (oracle.hpp:47-114) of instance k on the GPU:
         (points[time, eff_energy_mj, code], freq_mhz[point, computation])."""

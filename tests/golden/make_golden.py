@@ -18,6 +18,12 @@ Fixtures (JSON lines, gzip):
 
   artifacts.jsonl.gz  frontier.csv + schedule_<k>.json bytes (serde.hpp:194-257)
   brute.jsonl.gz      brute_force_frontier exact frontiers (oracle.hpp:47-114)
+  getnext.jsonl.gz    get_next_schedule from caller schedules outside the
+                      curve intervals (tables widened around the start)
+  batch5.jsonl.gz     config-5 batch instances: the largest 16x256 walks and
+                      mid-size walks in full, 300-step prefixes of the 16
+                      stratified samples ("batch5", opt-in: ~2 h on 6 cores;
+                      BATCH5_FROM=dir collects the outputs of earlier runs)
   walks_large.jsonl.gz  full-size reference walks of G9 configs 3 (8x128) and
                       4 (16x128) -- ~30 min of reference CPU time ("large")
 
@@ -77,9 +83,87 @@ def main():
         write("artifacts.jsonl.gz", run("artifacts", "1", *art) + run("artifacts", "10", "config:1", "diamond"))
     if "large" in parts:
         write("walks_large.jsonl.gz", run("walkcheck", "config:3") + run("walkcheck", "config:4"))
+    if "batch5" in parts:  # opt-in: hours of reference CPU time
+        batch5(os.environ.get("BATCH5_FROM"))
+    if "getnext" in parts:
+        write("getnext.jsonl.gz", run("getnext", "1000", *getnext_cases(walk_specs)))
     if "brute" in parts:
         small = [w for w in walk_specs if w.startswith(("grid:", "diamond", "lone", "cubic:"))][:60]
         write("brute.jsonl.gz", run("brute", *small, "config:1"))
+
+
+# Config-5 goldens (the headline batch): the two largest
+# 16x256 walks in full (~1.5-2 h of reference CPU each), three mid-size walks
+# in full, the first 300 steps of the 16 stratified sample instances.
+BATCH5_FULL = ["batch:3284", "batch:2404", "batch:2641", "batch:150", "batch:3496"]
+BATCH5_PREFIX = [f"batch:{i}" for i in range(0, 4096, 256)]
+
+
+def strip_instance(line):
+    """The batch instances are rebuilt natively (pb_batch_add_g9_batch, whose
+    generator test_g9_generator_matches_reference_instances pins): drop the
+    instance dump and curves to keep the fixture small."""
+    w = json.loads(line)
+    w.pop("instance", None)
+    w.pop("curves", None)
+    w.pop("wall_s", None)
+    return json.dumps(w, separators=(",", ":"))
+
+
+def batch5(from_dir=None):
+    """Runs the reference on every config-5 golden in parallel (or collects
+    outputs of earlier runs, one JSON line per walk, from from_dir/*.jsonl)."""
+    lines = []
+    if from_dir:
+        import glob
+        for path in sorted(glob.glob(os.path.join(from_dir, "*.jsonl"))):
+            lines += [strip_instance(x) for x in open(path) if x.startswith('{"spec":"batch:')]
+    else:
+        procs = [subprocess.Popen([DRIVER, "walk", s], stdout=subprocess.PIPE, text=True) for s in BATCH5_FULL]
+        procs.append(subprocess.Popen([DRIVER, "walkprefix", "300", *BATCH5_PREFIX], stdout=subprocess.PIPE, text=True))
+        for p in procs:
+            out, _ = p.communicate()
+            lines += [strip_instance(x) for x in out.splitlines() if x.strip()]
+    order = {s: i for i, s in enumerate(BATCH5_FULL + BATCH5_PREFIX)}
+    lines.sort(key=lambda x: order.get(json.loads(x)["spec"], 99))
+    write("batch5.jsonl.gz", lines)
+
+
+def getnext_cases(walk_specs):
+    """get_next_schedule from caller schedules whose planned times lie
+    anywhere in [t_min - 3 tau, t_max + 3 tau] (also off the tau grid): the
+    curve is evaluated outside its fitted interval (costmodel.hpp:47)."""
+    import random
+    rng = random.Random(2312)
+    specs = ["diamond", "lone:1000:9000:3000:5000", "config:1"]
+    specs += [w for w in walk_specs if w.startswith(("grid:", "cubic:", "g9:"))][::3]
+    with gzip.open(os.path.join(HERE, "walks.jsonl.gz"), "rt") as f:
+        walks = {w["spec"]: w for w in map(json.loads, f)}
+    args = []
+    for spec in specs:
+        w = walks[spec]
+        cls = {(c["stage"], c["kind"]): c for c in w["curves"]}
+        comps = w["instance"]["comps"]
+        rng_lo_hi = []
+        for stage, kind, _ in comps:
+            c = cls[(stage, kind)]
+            rng_lo_hi.append((c["pareto"][0][1],) * 2 if c["constant"] else (c["t_min"], c["t_max"]))
+        for rep in range(6):
+            # rep 0-1: every computation shifted above t_max; rep 2-5: the
+            # seed (t_max) with a few computations moved below t_min or
+            # above t_max; odd reps off the tau grid
+            if rep < 2:
+                k = rng.randint(1, 3)
+                start = [hi + k * 1000 for lo, hi in rng_lo_hi]
+            else:
+                start = [hi for lo, hi in rng_lo_hi]
+                for i in rng.sample(range(len(comps)), min(len(comps), rng.randint(1, 3))):
+                    lo, hi = rng_lo_hi[i]
+                    start[i] = lo - rng.randint(1, 3) * 1000 if rng.random() < 0.6 else hi + rng.randint(1, 3) * 1000
+            if rep % 2:
+                start = [t + rng.randint(-400, 400) for t in start]
+            args += [spec, ",".join(str(max(1, t)) for t in start)]
+    return args
 
 
 if __name__ == "__main__":

@@ -23,12 +23,22 @@ def _eff(sum_e, sum_t, watts, q):
     return float(sum_e) - watts * float(sum_t) * float(q) * 1e-3
 
 
-def check_walk_against(batch, k, w, watts, q, full=True):
+def check_walk_against(batch, k, w, watts, q, full=True, hash_points=None):
+    """Instance k of a run batch against reference walk w (ref_driver walk
+    JSON).  A prefix golden (reason "max_steps", ref_driver walkprefix) is
+    compared on its steps only.  full: the schedule hash of every point;
+    else of hash_points (if given)."""
     s = batch.summary(k)
     assert s.status == 0
-    assert pb.STOP_NAMES[s.stop] == w["reason"], (w["spec"], pb.STOP_NAMES[s.stop], w["reason"])
-    assert (s.t_min, s.t_star, s.steps) == (w["t_min"], w["t_star"], w["steps"]), w["spec"]
-    pts = batch.points(k)
+    assert s.n_table_misses == 0, w["spec"]  # every curve value came from the host (libm) tables
+    assert (s.t_min, s.t_star) == (w["t_min"], w["t_star"]), w["spec"]
+    nst = w["steps"]
+    if w["reason"] == "max_steps":
+        assert s.steps >= nst, (w["spec"], s.steps, nst)
+    else:
+        assert pb.STOP_NAMES[s.stop] == w["reason"], (w["spec"], pb.STOP_NAMES[s.stop], w["reason"])
+        assert s.steps == nst, w["spec"]
+    pts = batch.points(k)[:nst + 1]
     assert pts["t_planned"].tolist() == w["t_planned"], w["spec"]
     assert pts["t_realized"].tolist() == w["t_realized"], w["spec"]
     assert pts["sum_planned_e"].tolist() == w["sum_planned_e"], w["spec"]
@@ -36,23 +46,24 @@ def check_walk_against(batch, k, w, watts, q, full=True):
     assert pts["cut_cost"][1:].tolist() == w["cut_cost"], w["spec"]
     assert pts["step_size"][1:].tolist() == w["step_size"], w["spec"]
     ids, _ = batch.deltas(k)
-    for j in range(1, s.steps + 1):
+    for j in range(1, nst + 1):
         p = pts[j]
         seg = ids[p["id_begin"]:p["id_begin"] + p["n_sped"] + p["n_slowed"]]
         assert [int(x) - 1 for x in seg if x > 0] == w["sped"][j - 1], (w["spec"], j)
         assert [int(-x) - 1 for x in seg if x < 0] == w["slowed"][j - 1], (w["spec"], j)
-    for j in range(s.steps + 1):
+    for j in range(nst + 1):
         ep = _eff(pts["sum_planned_e"][j], pts["sum_planned_t"][j], watts, q)
         er = _eff(pts["sum_realized_e"][j], pts["sum_realized_t"][j], watts, q)
         assert abs(ep - w["eff_planned"][j]) <= REL * max(1.0, abs(w["eff_planned"][j]))
         assert abs(er - w["eff_realized"][j]) <= REL * max(1.0, abs(w["eff_realized"][j]))
     if full:
-        for j in range(s.steps + 1):
-            d = batch.schedule(k, j)
-            h = port.schedule_hash(d.planned_t, d.planned_e, d.freq_mhz, d.realized_t, d.realized_e)
-            assert h == w["hash"][j], (w["spec"], j)
-            assert d.eff_planned_mj == w["eff_planned"][j]
-            assert d.eff_realized_mj == w["eff_realized"][j]
+        hash_points = range(nst + 1)
+    for j in hash_points or ():
+        d = batch.schedule(k, j)
+        h = port.schedule_hash(d.planned_t, d.planned_e, d.freq_mhz, d.realized_t, d.realized_e)
+        assert h == w["hash"][j], (w["spec"], j)
+        assert d.eff_planned_mj == w["eff_planned"][j]
+        assert d.eff_realized_mj == w["eff_realized"][j]
 
 
 def test_every_golden_walk_in_one_batch(walks):
@@ -246,6 +257,29 @@ def test_lone_get_next_schedule():
         pb.get_next_schedule(dag, seed, m, 0)
     with pytest.raises(ValueError):
         pb.discover_frontier(dag, m, 0)
+
+
+def test_get_next_from_schedules_outside_the_curve_interval(walks):
+    """get_next_schedule (frontier.hpp:90-135) from caller schedules with
+    planned times below t_min / above t_max, on and off the tau grid: the
+    reference evaluates ExpCurve::eval there (costmodel.hpp:47); the device
+    reads the host tables, widened around the start schedule, and must
+    reproduce the step exactly (golden: ref_driver getnext)."""
+    from conftest import load_golden
+    cases = load_golden("getnext.jsonl.gz")
+    assert sum("cut_cost" in c for c in cases) > 100
+    for c in cases:
+        dag, model, _ = instance_from_golden(walks[c["spec"]])
+        cur = pb.EnergySchedule(0, list(c["start"]), list(c["start_e"]))
+        info = pb.StepInfo()
+        nxt = pb.get_next_schedule(dag, cur, model, c["tau"], info)
+        if "cut_cost" not in c:
+            assert nxt is None, c
+            continue
+        assert nxt is not None, c
+        assert (info.cut_cost, info.sped_up, info.slowed_down) == (c["cut_cost"], c["sped"], c["slowed"]), c
+        assert nxt.planned_t == c["planned_t"] and nxt.planned_e == c["planned_e"], c
+        assert nxt.t_planned == c["t_planned"] and nxt.eff_planned_mj == c["eff_planned"], c
 
 
 def test_diamond_step_by_step():
@@ -516,3 +550,49 @@ def test_full_size_configs_3_and_4_bit_exact():
     b.run(0)
     for k, (w, model) in enumerate(zip(recs, meta)):
         check_walk_against(b, k, w, model.blocking_watts, model.quantum_us, full=True)
+
+
+@pytest.fixture(scope="module")
+def batch5():
+    """The headline workload: the whole config-5 batch (4096 instances), as
+    bench.py runs it -- the LPT head on the cooperative kernel, the rest on
+    walker warps, one launch."""
+    b = pb.FrontierBatch()
+    b.add_g9_batch(0, 4096)
+    b.run(0)
+    return b
+
+
+def test_config5_batch_bit_exact_vs_reference(batch5):
+    """Config-5 instances against the unmodified reference (golden
+    batch5.jsonl.gz, ref_driver walk / walkprefix): the largest 16x256 walks
+    in full (they run on the cooperative kernel with shared-memory parent
+    links and the split capacity pass), mid-size walks in full, and the first
+    300 steps of the 16 stratified sample instances (i = 0 mod 256)."""
+    from conftest import load_golden
+    gold = load_golden("batch5.jsonl.gz")
+    coop = 0
+    for w in gold:
+        k = int(w["spec"].split(":")[1])
+        n = len(w["t_planned"]) - 1
+        sample = sorted({0, 1, n // 3, n // 2, (2 * n) // 3, n})
+        check_walk_against(batch5, k, w, 75.0, 1, full=False, hash_points=sample)
+        if w["reason"] != "max_steps" and batch5.summary(k).warps > 1:
+            coop += 1
+    heavy = [w for w in gold if w["reason"] != "max_steps" and len(w["t_planned"]) > 6000]
+    assert all(batch5.summary(int(w["spec"].split(":")[1])).warps > 1 for w in heavy)
+    assert sum(w["reason"] == "max_steps" for w in gold) >= 16
+
+
+def test_config5_batch_is_deterministic(batch5):
+    """Every instance of the 4096 batch: status ok, no table miss, and the
+    same results (digest of points + delta records) on a second launch --
+    the minimal min cut is unique, so the walk must not depend on timing."""
+    n = len(batch5)
+    first = [batch5.digest(k) for k in range(n)]
+    for k in range(n):
+        s = batch5.summary(k)
+        assert s.status == 0 and s.n_table_misses == 0, k
+    batch5.launch()
+    batch5.fetch()
+    assert [batch5.digest(k) for k in range(n)] == first

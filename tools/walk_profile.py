@@ -41,7 +41,7 @@ def profile(name):
     N.check(N.lib.pb_batch_profile(b._h, N.ptr(prof, C.c_int64), 16))
     st = b.stats()
     steps = sum(b.summary(k).steps for k in range(len(b)))
-    bad = [(k, b.summary(k).status, b.summary(k).n_extrapolated, b.summary(k).steps) for k in range(len(b)) if b.summary(k).status]
+    bad = [(k, b.summary(k).status, b.summary(k).n_table_misses, b.summary(k).steps) for k in range(len(b)) if b.summary(k).status]
     walk = max(prof[7], 1)
     print(f"== {name}: kernel {ms:.1f} ms, {steps} steps, {ms * 1e3 / max(steps, 1):.1f} us/step, wall {time.time() - t:.1f}s")
     print("   cycles share: " + ", ".join(f"{NAMES[i]} {prof[i] / walk:.1%}" for i in range(7)))
