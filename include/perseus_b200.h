@@ -290,6 +290,9 @@ pb_status pb_batch_add_g9_batch(pb_batch* b, int32_t first, int32_t count, int64
 /* Config-5 instances idx[0..count) (any order, repeats allowed), built in
  * parallel, appended in list order (an LPT shard of the batch). */
 pb_status pb_batch_add_g9_indices(pb_batch* b, const int32_t* idx, int32_t count, int64_t tau, int32_t threads);
+/* Sets pb_instance_desc.max_steps of every instance already added (a capped
+ * sample: each walk stops after that many steps). */
+pb_status pb_batch_set_max_steps(pb_batch* b, int32_t max_steps);
 /* The 9 (freq, time, energy) points of a stage base (descending frequency). */
 pb_status pb_g9_profile(int32_t b, int32_t backward, int64_t tau, int32_t* freq, int64_t* time,
                         int64_t* energy);

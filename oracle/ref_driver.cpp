@@ -17,6 +17,8 @@
 //   bench <threads> <spec>...  wall-time of discover_frontier over a thread
 //                            pool (one instance per task, LPT order given)
 //   fit <spec>               CostModel curves (bit patterns) of an instance
+//   budget <s> <threads> <spec>...   walks bounded by seconds per instance
+//   capped <k> <threads> <spec>...   walks bounded by k steps per instance
 //   artifacts <quantum> <spec>...
 //                            frontier.csv + schedule_<k>.json bytes
 //                            (serde.hpp frontier_csv / schedule_json dump(2))
@@ -613,8 +615,13 @@ int mode_brute(int argc, char** argv) {
   return 0;
 }
 
-int mode_budget(int argc, char** argv) {
-  const double budget = std::stod(argv[2]);
+// budget <seconds> <threads> <spec>...: each instance walked for at most
+// that many seconds; capped <steps> <threads> <spec>...: for at most that
+// many steps (a deterministic sample: the GPU arm walks the identical
+// capped sample with pb_instance_desc.max_steps).
+int mode_budget(int argc, char** argv, bool by_steps) {
+  const double budget = by_steps ? 1e300 : std::stod(argv[2]);
+  const long long max_steps = by_steps ? std::stoll(argv[2]) : -1;
   const int threads = std::max(1, std::stoi(argv[3]));
   std::vector<std::string> specs;
   for (int i = 4; i < argc; ++i) specs.push_back(argv[i]);
@@ -638,7 +645,8 @@ int mode_budget(int argc, char** argv) {
         long long p = 1, k = 0;
         bool done = true;
         while (cur.t_planned > t_min) {
-          if (std::chrono::duration<double>(std::chrono::steady_clock::now() - s0).count() > budget) {
+          if ((max_steps >= 0 && k >= max_steps) ||
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - s0).count() > budget) {
             done = false;
             break;
           }
@@ -657,9 +665,10 @@ int mode_budget(int argc, char** argv) {
     });
   for (auto& th : pool) th.join();
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  std::printf("{\"instances\":%zu,\"threads\":%d,\"budget_s\":%.3f,\"points\":%lld,\"steps\":%lld,"
-              "\"complete\":%lld,\"wall_s\":%.6f}\n",
-              insts.size(), threads, budget, points.load(), steps.load(), complete.load(), wall);
+  std::printf("{\"instances\":%zu,\"threads\":%d,\"budget_s\":%.3f,\"max_steps\":%lld,\"points\":%lld,"
+              "\"steps\":%lld,\"complete\":%lld,\"wall_s\":%.6f}\n",
+              insts.size(), threads, by_steps ? 0.0 : budget, max_steps, points.load(), steps.load(),
+              complete.load(), wall);
   (void)argc;
   return 0;
 }
@@ -773,7 +782,8 @@ int main(int argc, char** argv) {
     if (mode == "flow") return mode_flow(argc, argv);
     if (mode == "slack") return mode_slack(argc, argv);
     if (mode == "bench") return mode_bench(argc, argv);
-    if (mode == "budget") return mode_budget(argc, argv);
+    if (mode == "budget") return mode_budget(argc, argv, false);
+    if (mode == "capped") return mode_budget(argc, argv, true);
     if (mode == "savings") return mode_savings(argc, argv);
     if (mode == "artifacts") return mode_artifacts(argc, argv);
     if (mode == "brute") return mode_brute(argc, argv);

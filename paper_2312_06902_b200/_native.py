@@ -185,6 +185,7 @@ def _load() -> C.CDLL:
         "pb_batch_add_g9_batch": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, C.c_int32]),
         "pb_batch_add_g9_indices": (C.c_int, [P, i32p, C.c_int32, C.c_int64, C.c_int32]),
         "pb_batch_digest": (C.c_int, [P, C.c_int32, C.POINTER(C.c_uint64)]),
+        "pb_batch_set_max_steps": (C.c_int, [P, C.c_int32]),
         "pb_batch_brute_force": (C.c_int, [P, C.c_int32, C.c_double, C.c_int32, C.POINTER(ExactPoint), i32p,
                                            C.c_int32, i32p]),
         "pb_batch_schedule_json": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, C.c_char_p, C.c_int64, i64p]),
@@ -217,7 +218,7 @@ EXPORTED = (
     "pb_batch_stats", "pb_batch_profile", "pb_batch_destroy", "pb_annotate_slack_batch", "pb_flow_min_cut_batch",
     "pb_g9_stage_bases", "pb_g9_batch_params", "pb_g9_profile", "pb_batch_add_g9", "pb_batch_straggler",
     "pb_batch_frontier_csv", "pb_batch_schedule_json", "pb_batch_brute_force",
-    "pb_batch_add_g9_batch", "pb_batch_add_g9_indices", "pb_batch_digest",
+    "pb_batch_add_g9_batch", "pb_batch_add_g9_indices", "pb_batch_digest", "pb_batch_set_max_steps",
 )
 
 

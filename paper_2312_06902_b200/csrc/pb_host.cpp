@@ -2067,6 +2067,23 @@ pb_status pb_batch_add_g9_indices(pb_batch* b, const int32_t* idx, int32_t count
   return PB_OK;
 }
 
+pb_status pb_batch_set_max_steps(pb_batch* b, int32_t max_steps) {
+  if (!b) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
+  if (max_steps < -1) return fail(PB_ERR_INVALID_ARGUMENT, "max_steps must be >= -1");
+  for (auto& h : b->insts) {
+    h.max_steps = max_steps;
+    if (h.start.empty()) {  // sizing estimate as in validate_and_derive
+      h.est_steps = std::max<int64_t>(0, h.t_star_est - h.t_min_est) / h.tau + 2;
+      if (max_steps > 0) h.est_steps = std::min<int64_t>(h.est_steps, max_steps);
+    } else {
+      h.est_steps = std::max<int64_t>(1, max_steps);
+    }
+    h.work = static_cast<int64_t>(h.n + static_cast<int64_t>(h.edge_tail.size()) + 1) * h.est_steps;
+  }
+  b->have_results = false;
+  return PB_OK;
+}
+
 pb_status pb_batch_add_g9_batch(pb_batch* b, int32_t first, int32_t count, int64_t tau, int32_t threads) {
   if (!b || first < 0 || count < 0) return fail(PB_ERR_INVALID_ARGUMENT, "bad argument");
   std::vector<int32_t> idx(count);

@@ -133,6 +133,12 @@ class FrontierBatch:
         N.check(N.lib.pb_batch_stats(self._h, C.byref(s)))
         return s
 
+    def profile(self) -> np.ndarray:
+        """Per-phase device profile of the last launch (pb_batch_profile, 16 slots)."""
+        out = np.zeros(16, np.int64)
+        N.check(N.lib.pb_batch_profile(self._h, N.ptr(out, C.c_int64), 16))
+        return out
+
     def straggler(self, factors, pipelines: int, num_stages) -> np.ndarray:
         """straggler_savings (baselines.hpp:162-188) of every instance on the
         device-resident frontiers of the last run: rows[k, j] for factors[j]."""
@@ -159,6 +165,10 @@ class FrontierBatch:
         for i in idx.tolist():
             p = g9.batch_params(i)
             self._packed.append(_G9Meta(2 * p.stages * p.microbatches))
+
+    def set_max_steps(self, max_steps: int) -> None:
+        """Caps every instance's walk at max_steps steps (pb_batch_set_max_steps)."""
+        N.check(N.lib.pb_batch_set_max_steps(self._h, max_steps))
 
     def digest(self, k: int) -> int:
         """64-bit digest of instance k's results (pb_batch_digest)."""

@@ -596,3 +596,32 @@ def test_config5_batch_is_deterministic(batch5):
     batch5.launch()
     batch5.fetch()
     assert [batch5.digest(k) for k in range(n)] == first
+
+
+def test_run_multi_two_devices_matches_single(walks):
+    """pb_batch_run_multi LPT-shards a batch over a device list (here device
+    0 twice, two host threads): results stitched back in caller order, delta
+    pools and curve-table offsets rebased -- bit-identical to one device."""
+    specs = ["diamond", "config:1", "config:2"] + [s for s in walks if s.startswith(("grid:", "g9:"))][:30]
+
+    def build():
+        b = pb.FrontierBatch()
+        for s in specs:
+            dag, model, tau = instance_from_golden(walks[s])
+            b.add(dag, model, tau)
+        b.add_g9_indices([7, 300, 1234, 4000])
+        return b
+
+    one, two = build().run(0), build().run_multi([0, 0])
+    for k in range(len(specs) + 4):
+        assert two.summary(k).status == 0
+        assert two.digest(k) == one.digest(k), k
+        last = one.summary(k).steps
+        for j in {0, last // 2, last}:
+            a, c = one.schedule(k, j), two.schedule(k, j)
+            assert (a.planned_t, a.planned_e, a.freq_mhz, a.eff_planned_mj, a.eff_realized_mj) == \
+                (c.planned_t, c.planned_e, c.freq_mhz, c.eff_planned_mj, c.eff_realized_mj), (k, j)
+    for k, s in enumerate(specs):
+        check_walk_against(two, k, walks[s], walks[s]["instance"]["blocking_watts"],
+                           walks[s]["instance"]["quantum_us"], full=False, hash_points=[0])
+    assert two.frontier_csv(1) == one.frontier_csv(1)
