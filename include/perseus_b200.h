@@ -187,7 +187,7 @@ pb_status pb_batch_frontier_csv(const pb_batch* b, int32_t index, int64_t quantu
 pb_status pb_batch_schedule_json(const pb_batch* b, int32_t index, int32_t k, int64_t quantum_us,
                                  char* buf, int64_t cap, int64_t* len);
 /* Device-side timing/counters of the last run: kernel ms and work counters
- * (arc scans, node updates, push-relabel rounds). */
+ * (arc scans, node updates, BFS levels), and which walk kernels ran. */
 typedef struct {
   double kernel_ms;
   double h2d_ms;
@@ -196,15 +196,20 @@ typedef struct {
   int64_t d2h_bytes;
   int64_t arc_scans;
   int64_t node_updates;
-  int64_t rounds;
+  int64_t rounds; /* BFS levels (max-flow augmenting-path searches) */
   int64_t kernel_launches;
   int64_t comp_visits; /* longest-path node visits */
+  int64_t smem_walks;   /* instances walked shared-memory resident (walk_kernel_smem) */
+  int64_t wide_walks;   /* instances walked by cooperative multi-warp CTAs */
+  int64_t smem_region;  /* bytes of shared memory per resident walk (0: none) */
 } pb_run_stats;
 pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out);
-/* Raw per-phase profile of the last launch (cycles summed over CTAs, then
- * counts), n <= 16 slots: LP, capacities, phase A, phase B, global relabel,
- * cut BFS, update, whole walk, GR calls, GR levels, cut levels, rounds A,
- * rounds B, steps, max rounds of one push-relabel call, LP levels. */
+/* Raw per-phase profile of the last launch (cycles summed over walks, then
+ * counts), n <= 16 slots (pb_internal.h kPr*): cycles in the longest-path
+ * sweep, the capacity pass, max-flow phase A (feasibility repair), phase B
+ * (s->t augmentation), all BFS, all augmentations, the cut/tau update, the
+ * whole walk; then counts: phase-A BFS, phase-B BFS, BFS levels, augmenting
+ * paths, path arcs, steps, imbalanced nodes repaired, sweep levels. */
 pb_status pb_batch_profile(const pb_batch* b, int64_t* out, int32_t n);
 void pb_batch_destroy(pb_batch* b);
 

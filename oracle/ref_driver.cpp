@@ -523,6 +523,7 @@ int mode_bench(int argc, char** argv) {
   for (const auto& s : specs) insts.push_back(make_instance(s));
   std::atomic<size_t> next{0};
   std::atomic<long long> points{0}, steps{0};
+  std::vector<double> inst_s(insts.size(), 0.0);
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<std::thread> pool;
   for (int t = 0; t < threads; ++t)
@@ -530,15 +531,20 @@ int mode_bench(int argc, char** argv) {
       for (;;) {
         const size_t i = next.fetch_add(1);
         if (i >= insts.size()) return;
+        const auto w0 = std::chrono::steady_clock::now();
         const Frontier f = discover_frontier(insts[i].dag, insts[i].model, insts[i].tau);
+        inst_s[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
         points += static_cast<long long>(f.schedules.size());
         steps += f.steps;
       }
     });
   for (auto& th : pool) th.join();
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  std::printf("{\"instances\":%zu,\"threads\":%d,\"points\":%lld,\"steps\":%lld,\"wall_s\":%.6f}\n",
-              insts.size(), threads, points.load(), steps.load(), wall);
+  std::string per;
+  for (size_t i = 0; i < inst_s.size(); ++i) per += (i ? "," : "") + dbl(inst_s[i]);
+  std::printf("{\"instances\":%zu,\"threads\":%d,\"points\":%lld,\"steps\":%lld,\"wall_s\":%.6f,"
+              "\"instance_s\":[%s]}\n",
+              insts.size(), threads, points.load(), steps.load(), wall, per.c_str());
   return 0;
 }
 

@@ -135,6 +135,9 @@ class RunStats(C.Structure):
         ("rounds", C.c_int64),
         ("kernel_launches", C.c_int64),
         ("comp_visits", C.c_int64),
+        ("smem_walks", C.c_int64),
+        ("wide_walks", C.c_int64),
+        ("smem_region", C.c_int64),
     ]
 
 

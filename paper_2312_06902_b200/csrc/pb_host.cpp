@@ -363,6 +363,7 @@ struct DeviceRun {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   WidePlan wide;
+  int32_t smem_ctas = 0, smem_region = 0;  // > 0: every walk runs in walk_kernel_smem
   char* h_out = nullptr;  // pinned
   void release() {
     if (device < 0) return;
@@ -784,7 +785,7 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
     ck(cudaStreamCreateWithFlags(&R.stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&R.ev0), "event");
     ck(cudaEventCreate(&R.ev1), "event");
-    ck(cudaMalloc(&R.d_counter, 2 * sizeof(int32_t)), "malloc counter");
+    ck(cudaMalloc(&R.d_counter, 3 * sizeof(int32_t)), "malloc counter");
     ck(cudaMalloc(&R.d_counters, sizeof(pb::RunCounters)), "malloc counters");
     ck(cudaMalloc(&R.d_pool_cursor, sizeof(unsigned long long)), "malloc cursor");
   }
@@ -814,11 +815,34 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
     int sms = 0;
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
     R.wide = choose_wide(b, P.order, sms, std::max(1, pb::walk_slots_per_sm(R.ws)));
+    // Shared-memory-resident walks (walk_kernel_smem) whenever every walk of
+    // the batch gets its own CTA at once (PB_SMEM: -1 auto, 0 off, 1 force):
+    // one warp per SM-resident region instead of a warp of a 12-warp walker SM
+    R.smem_ctas = 0;
+    R.smem_region = 0;
+    // (an explicit PB_WIDE request keeps the cooperative kernel; PB_SMEM_REGION
+    // caps the region, e.g. to test partial placement)
+    const int mode = env_int("PB_SMEM", std::getenv("PB_WIDE") ? 0 : -1);
+    if (mode != 0) {
+      int64_t fmax = 0;
+      for (const pb::DevInst& d : P.dev)
+        fmax = std::max(fmax, pb::smem_footprint(d.n, d.V, d.E, d.ne, d.n_levels, d.n_snk));
+      if (const int cap_region = env_int("PB_SMEM_REGION", -1); cap_region >= 0)
+        fmax = std::min<int64_t>(fmax, cap_region);
+      int32_t region = 0, per = 0;
+      if (pb::smem_walk_plan(R.ws, fmax, &region, &per) != 0) throw CudaError("smem walk plan");
+      const int64_t cap = int64_t{sms} * per;
+      if (per > 0 && (mode == 1 || static_cast<int64_t>(N) <= cap)) {
+        R.smem_ctas = static_cast<int32_t>(std::min<int64_t>(static_cast<int64_t>(N), cap));
+        R.smem_region = region;
+        R.wide = WidePlan{};
+      }
+    }
   }
   // static bytes of the cooperative head walks (contiguous: LPT layout)
   R.wide_static_begin = N ? P.offs[P.order[0]][O_ORIG] : 0;
   R.wide_static_end = R.wide.n < static_cast<int32_t>(N) ? P.offs[P.order[R.wide.n]][O_ORIG] : P.stat_bytes;
-  R.slots = device_slots(device, static_cast<int64_t>(N) - R.wide.n, R.ws, R.wide);
+  R.slots = R.smem_ctas > 0 ? R.smem_ctas : device_slots(device, static_cast<int64_t>(N) - R.wide.n, R.ws, R.wide);
   ensure_device(R.d_ws, R.cap_ws, static_cast<size_t>(R.ws.stride) * (R.slots + R.wide.ctas), "malloc workspace");
   ensure_device(R.d_insts, R.cap_insts, sizeof(pb::DevInst) * N, "malloc insts");
   ensure_device(R.d_order, R.cap_order, sizeof(int32_t) * N, "malloc order");
@@ -861,7 +885,7 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   }
   if (R.device < 0) return fail(PB_ERR_LOGIC, "batch not prepared");
   ck(cudaSetDevice(R.device), "cudaSetDevice");
-  ck(cudaMemsetAsync(R.d_counter, 0, 2 * sizeof(int32_t), R.stream), "memset");
+  ck(cudaMemsetAsync(R.d_counter, 0, 3 * sizeof(int32_t), R.stream), "memset");
   ck(cudaMemsetAsync(R.d_counters, 0, sizeof(pb::RunCounters), R.stream), "memset");
   ck(cudaMemsetAsync(R.d_pool_cursor, 0, sizeof(unsigned long long), R.stream), "memset");
   pb::DeltaPool pool{R.d_pool_ids, R.d_pool_choice, R.d_pool_cursor, R.pool_cap};
@@ -888,9 +912,11 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
                    a.accessPolicyWindow.num_bytes, max_win, a.accessPolicyWindow.hitRatio);
   }
   ck(cudaEventRecord(R.ev0, R.stream), "record");
-  const int rc = pb::launch_walks(R.d_insts, static_cast<int32_t>(N), R.d_order, R.d_counter,
-                                  R.d_ws, R.ws, R.slots, R.d_counters, pool, R.wide.n, R.wide.ctas,
-                                  R.wide.warps, R.stream);
+  const int rc = R.smem_ctas > 0
+                     ? pb::launch_walks_smem(R.d_insts, static_cast<int32_t>(N), R.d_order, R.d_counter, R.d_ws,
+                                             R.ws, R.smem_region, R.smem_ctas, R.d_counters, pool, R.stream)
+                     : pb::launch_walks(R.d_insts, static_cast<int32_t>(N), R.d_order, R.d_counter, R.d_ws, R.ws,
+                                        R.slots, R.d_counters, pool, R.wide.n, R.wide.ctas, R.wide.warps, R.stream);
   if (rc != 0) throw CudaError(std::string("walk launch: ") + cudaGetErrorString(static_cast<cudaError_t>(rc)));
   ck(cudaEventRecord(R.ev1, R.stream), "record");
   ck(cudaStreamSynchronize(R.stream), "walk kernel");
@@ -904,7 +930,11 @@ pb_status launch_impl(pb_batch* b, double* kernel_ms) {
   b->stats.rounds = static_cast<int64_t>(rcnt.rounds);
   b->stats.comp_visits = static_cast<int64_t>(rcnt.comp_visits);
   for (int q = 0; q < pb::kPrSlots; ++q) b->prof[q] = static_cast<int64_t>(rcnt.prof[q]);
-  b->stats.kernel_launches += (R.wide.n > 0 ? 1 : 0) + (static_cast<int32_t>(N) > R.wide.n ? 1 : 0);
+  b->stats.smem_walks = R.smem_ctas > 0 ? static_cast<int64_t>(N) : 0;
+  b->stats.wide_walks = R.smem_ctas > 0 ? 0 : R.wide.n;
+  b->stats.smem_region = R.smem_ctas > 0 ? R.smem_region : 0;
+  b->stats.kernel_launches +=
+      R.smem_ctas > 0 ? 1 : (R.wide.n > 0 ? 1 : 0) + (static_cast<int32_t>(N) > R.wide.n ? 1 : 0);
   if (kernel_ms) *kernel_ms = ms;
   return PB_OK;
 }

@@ -300,6 +300,25 @@ int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order,
                  char* d_ws, const WsLayout& ws, int32_t slots, RunCounters* d_counters,
                  DeltaPool pool, int32_t n_wide, int32_t wide_ctas, int32_t wide_warps, void* stream);
 int walk_slots_per_sm(const WsLayout& ws);
+// Shared-memory-resident walks (walk_kernel_smem): one warp per CTA, each
+// CTA's region (bytes) holds as much of its walk's hot data as fits.
+// smem_walk_plan sizes the region for the largest footprint (smem_footprint)
+// and reports how many such CTAs fit per SM; the kernel pulls instances from
+// queue cursor d_counter[2].
+int smem_walk_plan(const WsLayout& ws, int64_t footprint, int32_t* region, int32_t* ctas_per_sm);
+int launch_walks_smem(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
+                      char* d_ws, const WsLayout& ws, int32_t region, int32_t ctas, RunCounters* d_counters,
+                      DeltaPool pool, void* stream);
+// Bytes a walk needs to be fully shared-memory resident (bind_smem's arrays,
+// 16 B aligned each).
+inline int64_t smem_footprint(int64_t n, int64_t V, int64_t E, int64_t ne, int64_t levels, int64_t nsnk) {
+  const int64_t a[] = {16 * E, 32 * E, 4 * (V + 1), 16 * V, 4 * V, 4 * (V + 2), 4 * (levels + 1), 8 * n, 16 * n,
+                       16 * n, 16 * n, 16 * n, 8 * n, E, n, 32 * n, 16 * n, 8 * ne, 8 * E, 8 * V, n, 4 * n,
+                       4 * nsnk, 4 * n};
+  int64_t t = 0;
+  for (int64_t x : a) t += align_up(x, 16);
+  return t;
+}
 int launch_flow_jobs(const DevFlowJob* d_jobs, int32_t count, char* d_ws, const WsLayout& ws,
                      int32_t slots, void* stream);
 int launch_slack_jobs(const DevInst* d_insts, const SlackOut* d_outs, int64_t* d_makespan,

@@ -46,6 +46,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
+#include <type_traits>
 
 #include "pb_internal.h"
 
@@ -65,6 +66,10 @@ constexpr int kLaneGroupLog2 = PB_LANE_GROUP_LOG2;  // >= 0 forces lanes per fro
 constexpr unsigned kFull = 0xffffffffu;
 constexpr long long kHuge = LLONG_MAX / 4;  // return-arc capacity (never binding)
 constexpr int kMaxEnds = 32;               // phase-B path ends kept per BFS
+#ifndef PB_BFS_PIPE
+#define PB_BFS_PIPE 1
+#endif
+constexpr bool kBfsPipe = PB_BFS_PIPE;     // BFS arc loads one round ahead
 typedef __int128 i128;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -114,7 +119,9 @@ __device__ __forceinline__ void red_add(long long* p, long long d) {
 
 __device__ __forceinline__ long long now() { return clock64(); }
 // L1 prefetch of the line holding p (global); no value returned, never faults.
-__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+// Generic form: a prefetch of a shared-memory address (the shared-memory-
+// resident walk, walk_kernel_smem) performs no operation.
+__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.L1 [%0];" ::"l"(p)); }
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -220,8 +227,9 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void atoms_and(uint32_t a, uint32_t m) {
   asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a), "r"(m) : "memory");
 }
-// Static incidence entry through the read-only path as one 16 B load.
-__device__ __forceinline__ int4 ldg_ient(const IEnt* p) { return __ldg(reinterpret_cast<const int4*>(p)); }
+// Static incidence entry as one 16 B load (generic: the incidence may be
+// staged in shared memory, walk_kernel_smem).
+__device__ __forceinline__ int4 ldg_ient(const IEnt* p) { return *reinterpret_cast<const int4*>(p); }
 __device__ __forceinline__ uint32_t atoms_or(uint32_t a, uint32_t m) {
   uint32_t old;
   asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(m) : "memory");
@@ -355,15 +363,28 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
       const int mine = fe.z > p ? (fe.z - p + g - 1) >> lg2 : 0;
       const int rounds = wmaxi(mine);
       arcs += mine;
+      // software pipeline: round r + 1's {ient, resid} pair is issued before
+      // round r is processed (nothing in a BFS writes resid), so a node's
+      // arcs cost one dependent round trip instead of one per round
+      int4 en = make_int4(0, 0, 0, 0);  // {other, packed twin, other_off, other_end}
+      long long wn = 0;
+      if (p < fe.z) {
+        en = ldg_ient(N.ient + p);
+        wn = N.resid[p];
+      }
       for (int r = 0; r < rounds; ++r, p += g) {
         const bool v = p < fe.z;
-        int4 e = make_int4(0, 0, 0, 0);  // {other, packed twin, other_off, other_end}
-        long long w = 0;
-        if (v) {
-          e = ldg_ient(N.ient + p);
-          w = N.resid[p];
+        if (!kBfsPipe && r > 0 && v) {  // A/B reference: each round loads its own pair
+          en = ldg_ient(N.ient + p);
+          wn = N.resid[p];
         }
-        const bool ok = w != 0 && w >= negS;
+        const int4 e = en;
+        const long long w = wn;
+        if (kBfsPipe && p + g < fe.z) {
+          en = ldg_ient(N.ient + p + g);
+          wn = N.resid[p + g];
+        }
+        const bool ok = v && w != 0 && w >= negS;  // e, w are stale past this lane's arcs
         const uint32_t m = ok ? 1u << (e.x & 31) : 0u;
         const uint32_t pw = lds32(N.s_pok + 4u * (e.x >> 5));  // issued beside the atomic
         const uint32_t o = atoms_or(N.s_bits + 4u * (e.x >> 5), m);
@@ -1766,6 +1787,108 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel_wide(const Dev
   flush_counters(C, ctr);
 }
 
+// ------------------------------------------- shared-memory-resident walks
+//
+// Small instances (and single walks, whose latency is what a caller of
+// discover_frontier sees) run from shared memory: the CTA's region holds a
+// copy of the instance record and, greedily in order of accesses per byte,
+// the walk's residuals, BFS log and static network (incidence entries, row
+// records, capacity records), then its longest-path state.  An array that
+// does not fit stays in global memory, so every instance can run here; the
+// walk code is unchanged (generic addressing).  Curve tables, outputs and
+// the cold lists (frontier overflow, touch / path lists) stay global.
+
+// 16 B-granular copy global -> shared (sources are 256 B aligned in the
+// static blob, whose sections are padded to 256 B, so the rounded-up tail
+// stays inside the blob).
+__device__ __forceinline__ void copy16(void* dst, const void* src, size_t bytes) {
+  const int4* s = reinterpret_cast<const int4*>(src);
+  int4* d = reinterpret_cast<int4*>(dst);
+  const size_t n = (bytes + 15) / 16;
+  for (size_t q = lane_id(); q < n; q += 32) d[q] = s[q];
+}
+
+// Places the walk's arrays into [region, region + cap): workspace arrays are
+// re-pointed (P), static arrays copied and re-pointed in the shared copy S of
+// the instance record.  Every lane computes the same layout.
+__device__ void bind_smem(DevInst& S, WsPtrs& P, char* region, size_t cap) {
+  char* cur = region;
+  char* const end = region + cap;
+  auto take = [&](size_t bytes) -> char* {
+    bytes = (bytes + 15) & ~static_cast<size_t>(15);
+    if (cur + bytes > end) return nullptr;
+    char* r = cur;
+    cur += bytes;
+    return r;
+  };
+  auto ws = [&](auto*& ptr, size_t bytes) {
+    if (char* r = take(bytes)) ptr = reinterpret_cast<std::remove_reference_t<decltype(ptr)>>(r);
+  };
+  auto st = [&](auto*& ptr, size_t bytes) {
+    if (char* r = take(bytes)) {
+      const void* src = ptr;
+      copy16(r, src, bytes);
+      __syncwarp();
+      ptr = reinterpret_cast<std::remove_reference_t<decltype(ptr)>>(r);
+    }
+  };
+  const size_t n = S.n, V = S.V, E = S.E, ne = S.ne;
+  // BFS: {incidence, residual} per arc, log + node index per discovery
+  ws(P.N.resid, 16 * E);
+  st(S.ient, 32 * E);
+  st(S.inc_off, 4 * (V + 1));
+  ws(P.N.lg, 16 * V);
+  ws(P.N.node_li, 4 * V);
+  ws(P.N.lvl_start, 4 * (V + 2));
+  // longest-path sweep + capacity pass
+  st(S.lvl_off, 4 * (S.n_levels + 1));
+  ws(P.W.durp, 8 * n);
+  ws(P.W.fin, 16 * n);
+  ws(P.W.tl, 16 * n);
+  st(S.frow, 16 * n);
+  st(S.brow, 16 * n);
+  ws(P.W.durr, 8 * n);
+  ws(P.W.ecrit, E);
+  ws(P.W.dirty, n);
+  st(S.crec, 32 * n);
+  ws(P.W.cap, 16 * n);
+  st(S.dep_nd, 8 * ne);
+  st(S.epos, 8 * E);
+  ws(P.N.bal, 8 * V);
+  ws(P.W.choice, n);
+  st(S.ilev, 4 * n);
+  st(S.snk, 4 * static_cast<size_t>(S.n_snk));
+  st(S.comp_class, 4 * n);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32, 1) walk_kernel_smem(const DevInst* insts, int n_inst, const int32_t* order,
+                                                          int32_t* counter, char* ws_base, WsLayout L,
+                                                          int region, RunCounters* ctr, DeltaPool pool) {
+  Counters C;
+  char* sm = my_smem(L, &C.prof);
+  const int per = 128 + 8 * kMaxEnds + L.smem_bytes;
+  DevInst* S = reinterpret_cast<DevInst*>(g_smem + per);
+  char* reg = g_smem + per + ((sizeof(DevInst) + 15) & ~static_cast<size_t>(15));
+  const WsPtrs G = bind_ws(ws_base + static_cast<size_t>(blockIdx.x) * L.stride, L, sm);
+  static_assert(sizeof(DevInst) % 8 == 0, "DevInst copy granularity");
+  for (;;) {
+    int k = 0;
+    if (lane_id() == 0) k = atomicAdd(counter + 2, 1);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= n_inst) break;
+    const long long* src = reinterpret_cast<const long long*>(&insts[order[k]]);
+    long long* dst = reinterpret_cast<long long*>(S);
+    for (int q = lane_id(); q < static_cast<int>(sizeof(DevInst) / 8); q += 32) dst[q] = src[q];
+    __syncwarp();
+    WsPtrs P = G;
+    bind_smem(*S, P, reg, static_cast<size_t>(region));
+    run_walk(*S, P.N, P.W, pool, C);
+    __syncwarp();
+  }
+  flush_counters(C, ctr);
+}
+
 // ------------------------------------------------------- straggler sweep
 
 // blocking_energy_mj (units.hpp:38-41)
@@ -2111,6 +2234,33 @@ int launch_walks(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order,
                                              slots, d_counters, pool, n_wide, wide_ctas);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
+  return static_cast<int>(cudaGetLastError());
+}
+
+int smem_walk_plan(const WsLayout& ws, int64_t footprint, int32_t* region, int32_t* ctas_per_sm) {
+  int dev = 0, optin = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  const int64_t base = 128 + 8 * kMaxEnds + ws.smem_bytes + ((sizeof(DevInst) + 15) & ~static_cast<size_t>(15));
+  const int64_t r = std::max<int64_t>(0, std::min<int64_t>(align_up(footprint, 16), optin - base));
+  const size_t sm = static_cast<size_t>(base + r);
+  set_smem(walk_kernel_smem, sm);
+  int blocks = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, walk_kernel_smem, 32, sm);
+  *region = static_cast<int32_t>(r);
+  *ctas_per_sm = blocks;
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_walks_smem(const DevInst* d_insts, int32_t n_inst, const int32_t* d_order, int32_t* d_counter,
+                      char* d_ws, const WsLayout& ws, int32_t region, int32_t ctas, RunCounters* d_counters,
+                      DeltaPool pool, void* stream) {
+  const size_t sm = 128 + 8 * kMaxEnds + ws.smem_bytes + ((sizeof(DevInst) + 15) & ~static_cast<size_t>(15)) +
+                    static_cast<size_t>(region);
+  set_smem(walk_kernel_smem, sm);
+  walk_kernel_smem<<<ctas, 32, sm, static_cast<cudaStream_t>(stream)>>>(d_insts, n_inst, d_order, d_counter, d_ws,
+                                                                        ws, region, d_counters, pool);
   return static_cast<int>(cudaGetLastError());
 }
 

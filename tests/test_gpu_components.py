@@ -1,5 +1,5 @@
-"""GPU parity of the component kernels behind the walk: the push-relabel min
-cut with lower bounds on arbitrary FlowGraphs (max_flow_lower_bounds +
+"""GPU parity of the component kernels behind the walk: the BFS-augmentation
+min cut with lower bounds on arbitrary FlowGraphs (max_flow_lower_bounds +
 min_cut_from_flow, flow.hpp:167-278) and the level-synchronous slack pass
 (annotate_slack, dag.hpp:233-286), against reference-produced corpora."""
 import ctypes as C

@@ -66,9 +66,16 @@ def check_walk_against(batch, k, w, watts, q, full=True, hash_points=None):
         assert d.eff_realized_mj == w["eff_realized"][j]
 
 
-def test_every_golden_walk_in_one_batch(walks):
+@pytest.mark.parametrize("smem,region", [("-1", None), ("0", None), ("1", "6000"), ("1", "0")])
+def test_every_golden_walk_in_one_batch(walks, monkeypatch, smem, region):
     """All 126 reference walks (golden instances, G9 configs 1-2, random grid
-    and cubic profiles with infeasible / infinite-cut stops) as ONE batch."""
+    and cubic profiles with infeasible / infinite-cut stops) as ONE batch:
+    shared-memory-resident walks (the automatic choice for a batch this
+    size), the global-memory walker, and shared-memory walks whose region
+    holds only part of the arrays (6000 B) or none of them."""
+    monkeypatch.setenv("PB_SMEM", smem)
+    if region is not None:
+        monkeypatch.setenv("PB_SMEM_REGION", region)
     b = pb.FrontierBatch()
     meta = []
     for spec, w in walks.items():
@@ -76,6 +83,10 @@ def test_every_golden_walk_in_one_batch(walks):
         b.add(dag, model, tau)
         meta.append((spec, model))
     b.run(0)
+    st = b.stats()
+    assert st.smem_walks == (0 if smem == "0" else len(meta)), (smem, st.smem_walks)
+    if region is not None:
+        assert st.smem_region <= int(region)
     for k, (spec, model) in enumerate(meta):
         check_walk_against(b, k, walks[spec], model.blocking_watts, model.quantum_us, full=spec != "config:2")
 

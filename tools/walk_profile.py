@@ -33,6 +33,8 @@ def profile(name):
     elif name.startswith("batch:"):
         for i in range(int(name.split(":")[1])):
             b.add_g9(g9.batch_params(i))
+    if os.environ.get("PB_PROFILE_MAX_STEPS"):  # step-capped walks (short ncu captures)
+        b.set_max_steps(int(os.environ["PB_PROFILE_MAX_STEPS"]))
     t = time.time()
     b.prepare(0)
     ms = b.launch()
@@ -48,7 +50,8 @@ def profile(name):
     S = max(prof[13], 1)
     print("   per step: " + ", ".join(f"{NAMES[i]} {prof[i] / S:.2f}" for i in range(8, 16)))
     print(f"   cycles/step {prof[7] / S:.0f}, cycles per bfs level {prof[4] / max(prof[10], 1):.0f}")
-    print(f"   arc_scans/step {st.arc_scans / S:.0f}, node_updates/step {st.node_updates / S:.0f}")
+    print(f"   arc_scans/step {st.arc_scans / S:.0f}, node_updates/step {st.node_updates / S:.0f}; "
+          f"smem walks {st.smem_walks} (region {st.smem_region} B), cooperative walks {st.wide_walks}")
     walks = sorted(((b.summary(k).walk_us, k) for k in range(len(b))), reverse=True)
     if len(walks) > 1:
         import heapq
