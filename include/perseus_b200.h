@@ -178,6 +178,14 @@ pb_status pb_batch_digest(const pb_batch* b, int32_t index, uint64_t* out);
 pb_status pb_batch_schedule(const pb_batch* b, int32_t index, int32_t k, int64_t* planned_t,
                             int64_t* planned_e, int32_t* freq_mhz, int64_t* realized_t,
                             int64_t* realized_e, double* eff_planned, double* eff_realized);
+/* Schedules first .. first + count - 1 of instance `index` in ONE
+ * incremental replay of the delta log (the whole Frontier of
+ * discover_frontier, frontier.hpp:166-189, without pb_batch_schedule's
+ * replay from point 0 per call): row q of each n-wide array (caller
+ * computation order) is schedule first + q; any pointer may be NULL. */
+pb_status pb_batch_schedules(const pb_batch* b, int32_t index, int32_t first, int32_t count,
+                             int64_t* planned_t, int64_t* planned_e, int32_t* freq_mhz, int64_t* realized_t,
+                             int64_t* realized_e, double* eff_planned, double* eff_realized);
 /* Optimizer artifacts from the delta log, byte-identical to the reference
  * writer (serde.hpp:250-257 frontier_csv; write_frontier_artifacts,
  * serde.hpp:304-316: schedule_json(s).dump(2) + "\n").  *len receives the
@@ -211,6 +219,11 @@ pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out);
  * whole walk; then counts: phase-A BFS, phase-B BFS, BFS levels, augmenting
  * paths, path arcs, steps, imbalanced nodes repaired, sweep levels. */
 pb_status pb_batch_profile(const pb_batch* b, int64_t* out, int32_t n);
+/* Drops every instance and result but keeps the handle's device context
+ * (stream, device and pinned buffers) for the next add/run: a persistent
+ * per-thread handle serves repeated single-instance calls (the drop-in's
+ * get_next_schedule) without re-allocating. */
+pb_status pb_batch_clear(pb_batch* b);
 void pb_batch_destroy(pb_batch* b);
 
 /* ---- straggler sweep on the device-resident frontiers -- */

@@ -193,36 +193,80 @@ struct B200Batch {
   B200Batch& operator=(const B200Batch&) = delete;
 };
 
-// Schedule k of a walked instance, materialized from the delta log.
-inline EnergySchedule b200_schedule(const pb_batch* b, int32_t index, int32_t k, int32_t n,
-                                    const pb_point& pt) {
-  EnergySchedule s;
-  s.schedule_id = k;
-  s.planned_t.resize(n);
-  s.planned_e.resize(n);
-  s.freq_mhz.resize(n);
-  s.realized_t.resize(n);
-  s.realized_e.resize(n);
-  b200_check(pb_batch_schedule(b, index, k, s.planned_t.data(), s.planned_e.data(), s.freq_mhz.data(),
-                               s.realized_t.data(), s.realized_e.data(), &s.eff_planned_mj,
-                               &s.eff_realized_mj));
-  s.t_planned = pt.t_planned;
-  s.t_realized = pt.t_realized;
-  return s;
+// The calling thread's persistent handle, emptied for each call: its device
+// context (stream, device and pinned buffers) is reused across calls, so a
+// loop of get_next_schedule calls packs and uploads one instance per call
+// and allocates nothing.  Distinct threads get distinct handles (and
+// streams), as the reference lets distinct jobs run concurrently.
+inline pb_batch* b200_handle() {
+  thread_local B200Batch b;
+  b200_check(pb_batch_clear(b.h));
+  return b.h;
+}
+
+// Walks instance `inst` (start schedule / step cap as set in its desc) on
+// the calling thread's handle; returns the summary, raising the reference's
+// exception for an error status.
+inline pb_frontier_summary b200_walk(pb_batch* h, B200Instance& inst) {
+  b200_check(pb_batch_add(h, &inst.desc, nullptr));
+  b200_check(pb_batch_run(h, b200_device()));
+  pb_frontier_summary sum;
+  b200_check(pb_batch_summary(h, 0, &sum));
+  if (sum.status != PB_OK) b200_raise(static_cast<pb_status>(sum.status));
+  return sum;
+}
+
+// Schedules [first, first + count) of a walked instance, materialized from
+// the delta log in one incremental replay (pb_batch_schedules) and appended
+// to out; iteration times are the device's (pb_point).
+inline void b200_schedules(const pb_batch* b, int32_t first, int32_t count, int32_t n, const pb_point* pts,
+                           std::vector<EnergySchedule>& out) {
+  const size_t cells = static_cast<size_t>(count) * static_cast<size_t>(n);
+  std::vector<int64_t> pt(cells), pe(cells), rt(cells), re(cells);
+  std::vector<int32_t> fr(cells);
+  std::vector<double> ep(count), er(count);
+  b200_check(pb_batch_schedules(b, 0, first, count, pt.data(), pe.data(), fr.data(), rt.data(), re.data(),
+                                ep.data(), er.data()));
+  for (int32_t q = 0; q < count; ++q) {
+    const size_t o = static_cast<size_t>(q) * static_cast<size_t>(n);
+    EnergySchedule s;
+    s.schedule_id = first + q;
+    s.planned_t.assign(pt.begin() + o, pt.begin() + o + n);
+    s.planned_e.assign(pe.begin() + o, pe.begin() + o + n);
+    s.freq_mhz.assign(fr.begin() + o, fr.begin() + o + n);
+    s.realized_t.assign(rt.begin() + o, rt.begin() + o + n);
+    s.realized_e.assign(re.begin() + o, re.begin() + o + n);
+    s.t_planned = pts[first + q].t_planned;
+    s.t_realized = pts[first + q].t_realized;
+    s.eff_planned_mj = ep[q];
+    s.eff_realized_mj = er[q];
+    out.push_back(std::move(s));
+  }
 }
 
 }  // namespace detail
 
-// Minimum-energy seed (frontier.hpp:73-83).
+// Minimum-energy seed (frontier.hpp:73-83): point 0 of a zero-step walk on
+// the GPU (planned times at each class's t_max, energies from the curve
+// tables, the device's longest path as T*).
 inline EnergySchedule min_energy_schedule(const NodeDag& dag, const CostModel& model) {
   EnergySchedule s;
-  for (const auto& comp : dag.computations) {
-    const auto& cm = model.require(class_of(comp));
-    const Quanta t = cm.is_constant ? cm.pareto.front().time : cm.curve->t_max;
-    s.planned_t.push_back(t);
-    s.planned_e.push_back(detail::planned_energy(cm, t));
+  const int32_t n = static_cast<int32_t>(dag.computations.size());
+  if (n == 0) {
+    detail::refresh_totals(dag, model, s);
+    return s;
   }
-  detail::refresh_totals(dag, model, s);
+  detail::B200Instance inst(dag, model, kDefaultTauUs);
+  inst.desc.max_steps = -1;  // no step: the seed only
+  pb_batch* h = detail::b200_handle();
+  (void)detail::b200_walk(h, inst);
+  pb_point p0;
+  detail::b200_check(pb_batch_points(h, 0, &p0, 1));
+  s.planned_t.resize(n);
+  s.planned_e.resize(n);
+  detail::b200_check(pb_batch_schedule(h, 0, 0, s.planned_t.data(), s.planned_e.data(), nullptr, nullptr,
+                                       nullptr, &s.eff_planned_mj, nullptr));
+  s.t_planned = p0.t_planned;
   return s;
 }
 
@@ -241,65 +285,74 @@ inline std::optional<EnergySchedule> get_next_schedule(const NodeDag& dag, const
   next.realized_t.clear();
   next.realized_e.clear();
   StepInfo st;
-  if (n > 0) {
-    detail::B200Instance inst(dag, model, tau);
-    inst.desc.start_planned_t = schedule.planned_t.data();
-    inst.desc.max_steps = 1;
-    detail::B200Batch b;
-    detail::b200_check(pb_batch_add(b.h, &inst.desc, nullptr));
-    detail::b200_check(pb_batch_run(b.h, detail::b200_device()));
-    pb_frontier_summary sum;
-    detail::b200_check(pb_batch_summary(b.h, 0, &sum));
-    if (sum.status != PB_OK) detail::b200_raise(static_cast<pb_status>(sum.status));
-    if (sum.stop == PB_STOP_INFEASIBLE || sum.stop == PB_STOP_INFINITE_CUT) return std::nullopt;
-    if (sum.steps != 1) throw std::logic_error("perseus-b200: single step did not run");
-    std::vector<pb_point> pts(2);
-    detail::b200_check(pb_batch_points(b.h, 0, pts.data(), 2));
-    std::vector<int32_t> ids(std::max(sum.n_ids, 1));
-    detail::b200_check(pb_batch_deltas(b.h, 0, ids.data(), nullptr, static_cast<int32_t>(ids.size())));
-    st.cut_cost = pts[1].cut_cost;
-    for (int32_t j = 0; j < sum.n_ids; ++j) {
-      const int comp = (ids[j] > 0 ? ids[j] : -ids[j]) - 1;
-      if (ids[j] > 0) {
-        next.planned_t[comp] -= tau;
-        st.sped_up.push_back(comp);
-      } else {
-        next.planned_t[comp] += tau;
-        st.slowed_down.push_back(comp);
-      }
-    }
-  } else {
+  if (n == 0) {
     // an empty DAG has no edge to cut: the reference's max flow is 0 < sentinel 1
     st.cut_cost = 0;
+    detail::refresh_totals(dag, model, next);
+    if (info) *info = std::move(st);
+    return next;
   }
-  for (int comp : st.sped_up)
-    next.planned_e[comp] = detail::planned_energy(model.require(class_of(dag.computations[comp])), next.planned_t[comp]);
-  for (int comp : st.slowed_down)
-    next.planned_e[comp] = detail::planned_energy(model.require(class_of(dag.computations[comp])), next.planned_t[comp]);
-  detail::refresh_totals(dag, model, next);
+  detail::B200Instance inst(dag, model, tau);
+  inst.desc.start_planned_t = schedule.planned_t.data();
+  inst.desc.max_steps = 1;
+  pb_batch* h = detail::b200_handle();
+  const pb_frontier_summary sum = detail::b200_walk(h, inst);
+  if (sum.stop == PB_STOP_INFEASIBLE || sum.stop == PB_STOP_INFINITE_CUT) return std::nullopt;
+  if (sum.steps != 1) throw std::logic_error("perseus-b200: single step did not run");
+  pb_point pts[2];
+  detail::b200_check(pb_batch_points(h, 0, pts, 2));
+  std::vector<int32_t> ids(std::max(sum.n_ids, 1));
+  detail::b200_check(pb_batch_deltas(h, 0, ids.data(), nullptr, static_cast<int32_t>(ids.size())));
+  // the device's step: new planned times and energies of the touched
+  // computations (curve tables), the new planned makespan
+  std::vector<int64_t> dev_t(n), dev_e(n);
+  detail::b200_check(pb_batch_schedule(h, 0, 1, dev_t.data(), dev_e.data(), nullptr, nullptr, nullptr, nullptr,
+                                       nullptr));
+  st.cut_cost = pts[1].cut_cost;
+  for (int32_t j = 0; j < sum.n_ids; ++j) {
+    const int comp = (ids[j] > 0 ? ids[j] : -ids[j]) - 1;
+    (ids[j] > 0 ? st.sped_up : st.slowed_down).push_back(comp);
+    next.planned_t[comp] = dev_t[comp];
+    next.planned_e[comp] = dev_e[comp];
+  }
+  next.t_planned = pts[1].t_planned;
+  // refresh_totals (frontier.hpp:64-67): untouched computations keep the
+  // caller's planned_e, so the index-order sum runs over the merged vector
+  next.eff_planned_mj = detail::effective_total(next.planned_e, next.planned_t, model.blocking, model.quantum_us);
   if (info) *info = std::move(st);
   return next;
 }
 
 // Snap to profiled frequencies (frontier.hpp:140-161): the last Pareto point
 // (ascending time) whose time fits the planned duration, else the fastest.
+// Runs on the GPU as a zero-step walk from schedule.planned_t: the device's
+// choice per computation, realized durations and realized makespan.
 inline EnergySchedule discretize(const EnergySchedule& schedule, const NodeDag& dag, const CostModel& model) {
   EnergySchedule out = schedule;
   out.freq_mhz.clear();
   out.realized_t.clear();
   out.realized_e.clear();
-  for (const auto& comp : dag.computations) {
-    const auto& pts = model.require(class_of(comp)).pareto;
-    const Quanta planned = schedule.planned_t[comp.id];
-    size_t pick = 0;
-    for (size_t j = 0; j < pts.size(); ++j)
-      if (pts[j].time <= planned) pick = j;
-    out.freq_mhz.push_back(pts[pick].freq_mhz);
-    out.realized_t.push_back(pts[pick].time);
-    out.realized_e.push_back(pts[pick].energy);
+  const int32_t n = static_cast<int32_t>(dag.computations.size());
+  if (n == 0) {
+    out.t_realized = detail::longest_path(dag, out.realized_t);
+    out.eff_realized_mj = 0;
+    return out;
   }
-  out.t_realized = detail::longest_path(dag, out.realized_t);
-  out.eff_realized_mj = detail::effective_total(out.realized_e, out.realized_t, model.blocking, model.quantum_us);
+  if (static_cast<int32_t>(schedule.planned_t.size()) < n)
+    throw std::invalid_argument("durations must cover every computation");
+  detail::B200Instance inst(dag, model, kDefaultTauUs);
+  inst.desc.start_planned_t = schedule.planned_t.data();
+  inst.desc.max_steps = -1;  // no step: discretize the start schedule only
+  pb_batch* h = detail::b200_handle();
+  (void)detail::b200_walk(h, inst);
+  pb_point p0;
+  detail::b200_check(pb_batch_points(h, 0, &p0, 1));
+  out.freq_mhz.resize(n);
+  out.realized_t.resize(n);
+  out.realized_e.resize(n);
+  detail::b200_check(pb_batch_schedule(h, 0, 0, nullptr, nullptr, out.freq_mhz.data(), out.realized_t.data(),
+                                       out.realized_e.data(), nullptr, &out.eff_realized_mj));
+  out.t_realized = p0.t_realized;
   return out;
 }
 
@@ -318,19 +371,18 @@ inline Frontier discover_frontier(const NodeDag& dag, const CostModel& model, Qu
     return f;
   }
   detail::B200Instance inst(dag, model, tau);
-  detail::B200Batch b;
-  detail::b200_check(pb_batch_add(b.h, &inst.desc, nullptr));
-  detail::b200_check(pb_batch_run(b.h, detail::b200_device()));
-  pb_frontier_summary sum;
-  detail::b200_check(pb_batch_summary(b.h, 0, &sum));
-  if (sum.status != PB_OK) detail::b200_raise(static_cast<pb_status>(sum.status));
+  pb_batch* h = detail::b200_handle();
+  const pb_frontier_summary sum = detail::b200_walk(h, inst);
   f.t_min = sum.t_min;
   f.t_star = sum.t_star;
   f.steps = sum.steps;
   std::vector<pb_point> pts(sum.steps + 1);
-  detail::b200_check(pb_batch_points(b.h, 0, pts.data(), sum.steps + 1));
+  detail::b200_check(pb_batch_points(h, 0, pts.data(), sum.steps + 1));
   f.schedules.reserve(sum.steps + 1);
-  for (int32_t k = 0; k <= sum.steps; ++k) f.schedules.push_back(detail::b200_schedule(b.h, 0, k, n, pts[k]));
+  // expand the delta log in chunks of ~16 MB of schedule data
+  const int32_t chunk = static_cast<int32_t>(std::max<int64_t>(1, (int64_t{1} << 24) / (36 * int64_t{n})));
+  for (int32_t k = 0; k <= sum.steps; k += chunk)
+    detail::b200_schedules(h, k, std::min(chunk, sum.steps + 1 - k), n, pts.data(), f.schedules);
   return f;
 }
 

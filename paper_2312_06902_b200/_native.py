@@ -193,6 +193,9 @@ def _load() -> C.CDLL:
                                            C.c_int32, i32p]),
         "pb_batch_schedule_json": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, C.c_char_p, C.c_int64, i64p]),
         "pb_batch_destroy": (None, [P]),
+        "pb_batch_clear": (C.c_int, [P]),
+        "pb_batch_schedules": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, i64p, i64p, i32p, i64p, i64p, f64p,
+                                         f64p]),
         "pb_annotate_slack_batch": (C.c_int, [C.c_int32, C.c_int32, i32p, i32p, i32p, i32p, i64p,
                                               i64p, i64p, u8p, i64p]),
         "pb_flow_min_cut_batch": (C.c_int, [C.c_int32, C.c_int32, i32p, i32p, i32p, i32p, i32p, i32p,
@@ -218,7 +221,8 @@ EXPORTED = (
     "pb_last_error", "pb_version", "pb_pareto_filter", "pb_fit_exp", "pb_batch_create", "pb_batch_add",
     "pb_batch_run", "pb_batch_prepare", "pb_batch_launch", "pb_batch_fetch", "pb_batch_size",
     "pb_batch_run_multi", "pb_batch_summary", "pb_batch_points", "pb_batch_deltas", "pb_batch_schedule",
-    "pb_batch_stats", "pb_batch_profile", "pb_batch_destroy", "pb_annotate_slack_batch", "pb_flow_min_cut_batch",
+    "pb_batch_stats", "pb_batch_profile", "pb_batch_destroy", "pb_batch_clear", "pb_batch_schedules",
+    "pb_annotate_slack_batch", "pb_flow_min_cut_batch",
     "pb_g9_stage_bases", "pb_g9_batch_params", "pb_g9_profile", "pb_batch_add_g9", "pb_batch_straggler",
     "pb_batch_frontier_csv", "pb_batch_schedule_json", "pb_batch_brute_force",
     "pb_batch_add_g9_batch", "pb_batch_add_g9_indices", "pb_batch_digest", "pb_batch_set_max_steps",

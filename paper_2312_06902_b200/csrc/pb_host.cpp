@@ -409,6 +409,53 @@ struct pb_batch {
   int64_t prof[pb::kPrSlots] = {};
   char* h_static = nullptr;  // pinned staging of the packed static blob (reused)
   size_t h_static_cap = 0;
+  // E(t) = a exp(b t) + c per curve over a contiguous range [lo, lo + size),
+  // grown on demand (costmodel.hpp:47: same expression and libm)
+  struct CurveCache {
+    int64_t lo = 0;
+    std::vector<double> v;
+  };
+  std::map<std::array<uint64_t, 3>, CurveCache> curve_cache;
+  size_t curve_cache_values = 0;
+  static std::array<uint64_t, 3> curve_id(double a, double b, double c) {
+    uint64_t x, y, z;
+    std::memcpy(&x, &a, 8);
+    std::memcpy(&y, &b, 8);
+    std::memcpy(&z, &c, 8);
+    return {x, y, z};
+  }
+  int64_t curve_lo(double a, double b, double c) const { return curve_cache.at(curve_id(a, b, c)).lo; }
+  const std::vector<double>& curve_values(double a, double b, double c, int64_t lo, int64_t hi) {
+    if (curve_cache_values > (size_t{1} << 26)) {  // bound the cache (~512 MB)
+      curve_cache.clear();
+      curve_cache_values = 0;
+    }
+    auto eval = [&](int64_t t) { return a * std::exp(b * static_cast<double>(t)) + c; };
+    auto ins = curve_cache.emplace(curve_id(a, b, c), CurveCache{});
+    CurveCache& cc = ins.first->second;
+    if (ins.second || cc.v.empty()) {
+      cc.lo = lo;
+      cc.v.resize(hi - lo + 1);
+      for (int64_t t = lo; t <= hi; ++t) cc.v[t - lo] = eval(t);
+      curve_cache_values += cc.v.size();
+      return cc.v;
+    }
+    const int64_t clo = cc.lo, chi = cc.lo + static_cast<int64_t>(cc.v.size()) - 1;
+    if (lo < clo) {
+      std::vector<double> head(clo - lo);
+      for (int64_t t = lo; t < clo; ++t) head[t - lo] = eval(t);
+      cc.v.insert(cc.v.begin(), head.begin(), head.end());
+      cc.lo = lo;
+      curve_cache_values += head.size();
+    }
+    if (hi > chi) {
+      const size_t old = cc.v.size();
+      cc.v.resize(old + (hi - chi));
+      for (int64_t t = chi + 1; t <= hi; ++t) cc.v[t - cc.lo] = eval(t);
+      curve_cache_values += hi - chi;
+    }
+    return cc.v;
+  }
   ~pb_batch() {
     run.release();
     if (h_static) cudaFreeHost(h_static);
@@ -561,9 +608,11 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
         const int64_t span = thi - tlo + 1;
         if (span > (int64_t{1} << 27)) throw std::length_error("curve interval too long to tabulate");
         b->tables.resize(b->tables.size() + span);
-        // ExpCurve::eval (costmodel.hpp:47), same expression and libm
-        for (int64_t t = tlo; t <= thi; ++t)
-          b->tables[at + (t - tlo)] = a * std::exp(bb * static_cast<double>(t)) + cc;
+        // ExpCurve::eval (costmodel.hpp:47), same expression and libm; values
+        // persist in the handle's curve cache across runs and pb_batch_clear
+        // (a get_next_schedule chain re-tabulates only the newly reached times)
+        const std::vector<double>& v = b->curve_values(a, bb, cc, tlo, thi);
+        std::memcpy(b->tables.data() + at, v.data() + (tlo - b->curve_lo(a, bb, cc)), sizeof(double) * span);
         it = table_of.emplace(key, at).first;
       }
       b->cls_tab[k][c] = it->second + (lo - tlo);  // offset of E(t_min)
@@ -1103,6 +1152,28 @@ pb_status pb_batch_create(pb_batch** out) {
 
 void pb_batch_destroy(pb_batch* b) { delete b; }
 
+pb_status pb_batch_clear(pb_batch* b) {
+  if (!b) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
+  // drop the instances and results; keep the device context (stream, device
+  // and pinned buffers), which the next run reuses while it fits
+  b->insts.clear();
+  b->tables.clear();
+  b->cls_tab.clear();
+  b->tab_margin.clear();
+  b->out_points.clear();
+  b->out_summary.clear();
+  b->cap_points.clear();
+  b->out.clear();
+  b->outp = nullptr;
+  b->pool_ids.clear();
+  b->pool_choice.clear();
+  b->pool_base.clear();
+  b->pool_cap = 0;
+  b->have_results = false;
+  b->stats = pb_run_stats{};
+  return PB_OK;
+}
+
 int32_t pb_batch_size(const pb_batch* b) { return b ? static_cast<int32_t>(b->insts.size()) : 0; }
 
 pb_status pb_batch_add(pb_batch* b, const pb_instance_desc* d, int32_t* out_index) {
@@ -1472,6 +1543,38 @@ pb_status pb_batch_schedule(const pb_batch* b, int32_t k, int32_t which, int64_t
   r.totals(effp, effr);
   if (eff_planned) *eff_planned = effp;
   if (eff_realized) *eff_realized = effr;
+  return PB_OK;
+}
+
+pb_status pb_batch_schedules(const pb_batch* b, int32_t k, int32_t first, int32_t count, int64_t* planned_t,
+                             int64_t* planned_e, int32_t* freq_mhz, int64_t* realized_t, int64_t* realized_e,
+                             double* eff_planned, double* eff_realized) {
+  if (count < 0) return fail(PB_ERR_INVALID_ARGUMENT, "negative count");
+  if (count == 0) return check_index(b, k, 0);
+  pb_status st = check_index(b, k, first);
+  if (st == PB_OK) st = check_index(b, k, first + count - 1);
+  if (st != PB_OK) return st;
+  Replay r(b, k);  // one incremental replay for the whole range
+  const HostInst& h = r.h;
+  const size_t n = static_cast<size_t>(h.n);
+  for (int32_t q = 0; q < count; ++q) {
+    r.advance_to(first + q);
+    const size_t o = static_cast<size_t>(q) * n;
+    for (int32_t i = 0; i < h.n; ++i) {
+      const int32_t p = h.cls_pt_off[h.comp_class[i]] + r.ch[i];
+      if (planned_t) planned_t[o + i] = r.pt[i];
+      if (planned_e) planned_e[o + i] = r.planned_energy(i);
+      if (freq_mhz) freq_mhz[o + i] = h.pt_freq[p];
+      if (realized_t) realized_t[o + i] = h.pt_time[p];
+      if (realized_e) realized_e[o + i] = h.pt_energy[p];
+    }
+    if (eff_planned || eff_realized) {
+      double effp, effr;
+      r.totals(effp, effr);
+      if (eff_planned) eff_planned[q] = effp;
+      if (eff_realized) eff_realized[q] = effr;
+    }
+  }
   return PB_OK;
 }
 

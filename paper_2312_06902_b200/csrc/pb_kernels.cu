@@ -1717,7 +1717,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel(const DevInst*
 // posted to the CTA's control block and expanded by all nw warps
 // (bfs_core<., true>); the other phases stay on warp 0.  The walk's shared
 // structures (frontier, bitsets, path ends) are warp 0's region.
-__global__ void __launch_bounds__(kBlock, kMinBlocks) walk_kernel_wide(const DevInst* insts, int n_wide,
+#ifndef PB_WIDE_MIN_BLOCKS
+#define PB_WIDE_MIN_BLOCKS kMinBlocks
+#endif
+__global__ void __launch_bounds__(kBlock, PB_WIDE_MIN_BLOCKS) walk_kernel_wide(const DevInst* insts, int n_wide,
                                                            const int32_t* order, int32_t* counter,
                                                            char* ws_base, WsLayout L, RunCounters* ctr,
                                                            DeltaPool pool) {

@@ -90,6 +90,13 @@ class FrontierBatch:
         self._packed.append(p)
         return idx.value
 
+    def clear(self) -> None:
+        """Drops every instance and result; the device context is kept
+        (pb_batch_clear)."""
+        N.check(N.lib.pb_batch_clear(self._h))
+        self._packed = []
+        self._ran = False
+
     def add_g9(self, p, tau: int = 1000) -> int:
         """Appends a G9 instance built natively (pb_batch_add_g9)."""
         idx = C.c_int32()
@@ -244,12 +251,30 @@ class FrontierBatch:
         return StepInfo(int(p["cut_cost"]), [int(x) - 1 for x in seg if x > 0],
                         [int(-x) - 1 for x in seg if x < 0])
 
+    def schedules(self, k: int, first: int = 0, count: int | None = None) -> list:
+        """Schedules first .. first + count - 1 of instance k in ONE incremental
+        replay of the delta log (pb_batch_schedules)."""
+        s = self.summary(k)
+        if count is None:
+            count = s.steps + 1 - first
+        n = self._packed[k].n
+        pt, pe, rt, re = (np.zeros((count, n), np.int64) for _ in range(4))
+        fr = np.zeros((count, n), np.int32)
+        ep, er = np.zeros(count), np.zeros(count)
+        N.check(N.lib.pb_batch_schedules(self._h, k, first, count, N.ptr(pt, C.c_int64), N.ptr(pe, C.c_int64),
+                                         N.ptr(fr, C.c_int32), N.ptr(rt, C.c_int64), N.ptr(re, C.c_int64),
+                                         N.ptr(ep, C.c_double), N.ptr(er, C.c_double)))
+        pts = self.points(k)
+        return [EnergySchedule(first + q, pt[q].tolist(), pe[q].tolist(), fr[q].tolist(), rt[q].tolist(),
+                               re[q].tolist(), int(pts[first + q]["t_planned"]), int(pts[first + q]["t_realized"]),
+                               float(ep[q]), float(er[q])) for q in range(count)]
+
     def frontier(self, k: int) -> Frontier:
         s = self.summary(k)
         N.raise_for_instance_status(s.status)
         f = Frontier(t_min=int(s.t_min), t_star=int(s.t_star), steps=int(s.steps),
                      stop=N.STOP_NAMES.get(s.stop, str(s.stop)))
-        f.schedules = [self.schedule(k, q) for q in range(s.steps + 1)]
+        f.schedules = self.schedules(k)
         return f
 
 

@@ -26,6 +26,12 @@ Fixtures (JSON lines, gzip):
                       BATCH5_FROM=dir collects the outputs of earlier runs)
   walks_large.jsonl.gz  full-size reference walks of G9 configs 3 (8x128) and
                       4 (16x128) -- ~30 min of reference CPU time ("large")
+  walks_phi.jsonl.gz  the config-4 straggler sweep (16x128, stage 8 slowed by
+                      phi in 1.05, 1.1, 1.2, 1.3, 1.5), full walks, instance
+                      dumps stripped (rebuilt by the native G9 builder) --
+                      ~15 min on 5 cores ("phi", opt-in)
+  savings_c4.jsonl.gz straggler_savings rows of configs 4 and 3 at the sweep
+                      factors (baselines.hpp:162-188) ("phi")
 
     python tests/golden/make_golden.py [walks|flow|slack|savings|artifacts ...]
   batch_small.jsonl.gz  small config-5 style G9 instances (summaries only)
@@ -55,6 +61,7 @@ def write(name, lines):
 
 
 SAVINGS_FACTORS = "1.0,1.05,1.1,1.2,1.3,1.5"  # SURVEY §8d config-4 straggler sweep
+PHI_SWEEP = ["1.05", "1.1", "1.2", "1.3", "1.5"]
 
 
 def main():
@@ -83,6 +90,17 @@ def main():
         write("artifacts.jsonl.gz", run("artifacts", "1", *art) + run("artifacts", "10", "config:1", "diamond"))
     if "large" in parts:
         write("walks_large.jsonl.gz", run("walkcheck", "config:3") + run("walkcheck", "config:4"))
+    if "phi" in parts:  # opt-in: ~15 min on 6 cores
+        procs = [subprocess.Popen([DRIVER, "walk", f"config:4:{p}"], stdout=subprocess.PIPE, text=True)
+                 for p in PHI_SWEEP]
+        sav = subprocess.Popen([DRIVER, "savings", "8", SAVINGS_FACTORS, "config:4", "config:3"],
+                               stdout=subprocess.PIPE, text=True)
+        lines = []
+        for p in procs:
+            out, _ = p.communicate()
+            lines += [strip_instance(x) for x in out.splitlines() if x.strip()]
+        write("walks_phi.jsonl.gz", lines)
+        write("savings_c4.jsonl.gz", [x for x in sav.communicate()[0].splitlines() if x.strip()])
     if "batch5" in parts:  # opt-in: hours of reference CPU time
         batch5(os.environ.get("BATCH5_FROM"))
     if "getnext" in parts:

@@ -36,3 +36,34 @@ def test_reference_acceptance_gates_through_the_b200_dropin():
     if os.path.exists(REF):
         ref, _ = gates(REF)
         assert {k: v[0] for k, v in got.items()} == {k: v[0] for k, v in ref.items()}
+
+
+CHAIN_B200 = os.path.join(ROOT, "oracle", "_ref", "dropin_chain_b200")
+CHAIN_REF = os.path.join(ROOT, "oracle", "_ref", "dropin_chain_ref")
+
+
+def _chain(binary, spec, steps):
+    import json
+    out = subprocess.run([binary, spec, str(steps)], capture_output=True, text=True, timeout=1200,
+                         check=True).stdout
+    recs = [json.loads(x) for x in out.splitlines() if x.strip()]
+    return [r for r in recs if r["what"] != "timing"], next(r for r in recs if r["what"] == "timing")
+
+
+@pytest.mark.skipif(not (os.path.exists(CHAIN_B200) and os.path.exists(CHAIN_REF)),
+                    reason="dropin_chain not built (make -C oracle acceptance)")
+@pytest.mark.parametrize("spec,steps", [("diamond", 50), ("config:1", 300), ("config:2", 1000)])
+def test_per_step_api_through_the_dropin_matches_reference(spec, steps):
+    """min_energy_schedule -> get_next_schedule -> discretize, chained through
+    the drop-in (every value from the device: the step's cut, the touched
+    computations' new planned times and energies, the planned makespan; the
+    discretized choice, realized times and makespan) and through the
+    unmodified reference: identical JSON lines, past T_min to the reference's
+    own stop (nullopt).  The timing of both is printed."""
+    got, t_b200 = _chain(CHAIN_B200, spec, steps)
+    ref, t_ref = _chain(CHAIN_REF, spec, steps)
+    assert len(got) == len(ref)
+    for a, b in zip(got, ref):
+        assert a == b, (a, b)
+    print(f"{spec}: {t_b200['steps']} get_next+discretize calls, drop-in {t_b200['wall_s']:.3f} s "
+          f"(get_next {t_b200['get_next_s']:.3f} s), reference {t_ref['wall_s']:.3f} s")

@@ -636,3 +636,54 @@ def test_run_multi_two_devices_matches_single(walks):
         check_walk_against(two, k, walks[s], walks[s]["instance"]["blocking_watts"],
                            walks[s]["instance"]["quantum_us"], full=False, hash_points=[0])
     assert two.frontier_csv(1) == one.frontier_csv(1)
+
+
+def test_config4_straggler_sweep_bit_exact_vs_reference():
+    """The config-4 straggler sweep (Bloom-like 16x128, stage 8
+    slowed by phi in 1.05 ... 1.5, each a separate instance) walked in full
+    against the unmodified reference (golden walks_phi: every point's times,
+    cut costs, ids and energies; schedule hashes at sampled points), and
+    straggler_savings (baselines.hpp:162-188) of configs 4 and 3 at the sweep
+    factors (golden savings_c4) on the device frontiers."""
+    from conftest import load_golden
+    walks_phi = load_golden("walks_phi.jsonl.gz")
+    sav = load_golden("savings_c4.jsonl.gz")
+    b = pb.FrontierBatch()
+    for w in walks_phi:
+        phi = float(w["spec"].split(":")[2])
+        b.add_g9(g9.named_config(4, phi))
+    b.add_g9(g9.named_config(4))
+    b.add_g9(g9.named_config(3))
+    b.run(0)
+    for k, w in enumerate(walks_phi):
+        n = w["steps"]
+        check_walk_against(b, k, w, 75.0, 1, full=False, hash_points=sorted({0, 1, n // 4, n // 2, n - 1, n}))
+    factors = [row["factor"] for row in sav[0]["rows"]]
+    P = sav[0]["pipelines"]
+    out = b.straggler(factors, P, [16] * len(walks_phi) + [16, 8])
+    for r, k in zip(sav, (len(walks_phi), len(walks_phi) + 1)):
+        assert r["spec"] == ("config:4", "config:3")[k - len(walks_phi)]
+        for j, ref in enumerate(r["rows"]):
+            got = out[k, j]
+            assert got["status"] == 0 and got["point"] == ref["point"], (r["spec"], ref["factor"])
+            scale = (P - 1) * abs(got["all_max_mj"])
+            assert abs(got["savings_mj"] - ref["savings_mj"]) <= 1e-9 * scale, (r["spec"], ref, got)
+            assert abs(got["savings_pct"] - ref["savings_pct"]) <= 1e-9 * 100, (r["spec"], ref, got)
+
+
+def test_schedules_range_matches_single_schedules(walks):
+    """pb_batch_schedules (one incremental replay for a range of points)
+    returns exactly what pb_batch_schedule returns point by point."""
+    w = walks["config:2"]
+    dag, model, tau = instance_from_golden(w)
+    b = pb.FrontierBatch()
+    b.add(dag, model, tau)
+    b.run(0)
+    s = b.summary(0)
+    rng = b.schedules(0, 5, 40)
+    for q, got in enumerate(rng):
+        assert got == b.schedule(0, 5 + q)
+    full = b.frontier(0).schedules
+    assert len(full) == s.steps + 1
+    for j in (0, s.steps // 2, s.steps):
+        assert full[j] == b.schedule(0, j)
