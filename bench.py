@@ -386,8 +386,10 @@ def run_ours(args):
         "data": "synthetic (G9 generator, SURVEY.md §8d)",
         "config": {"workload": desc, "instances_per_rank": len(b), "tau_us": 1000,
                    "l2": "no flush: per-walker workspaces + instance data exceed the 126 MB L2",
-                   "parallelism": f"instances LPT-ordered over {world} GPU(s): cooperative CTAs for the "
-                                  f"longest walks, one warp per walk for the rest"},
+                   "parallelism": (f"instances LPT-ordered over {world} GPU(s): " + (
+                       f"every walk shared-memory resident, one 1-warp CTA each ({st.smem_region} B region)"
+                       if st.smem_walks else
+                       f"{st.wide_walks} longest walks on 2-warp cooperative CTAs, one warp per walk for the rest"))},
         "iterations_per_s": total_steps * args.steps / t_dev,
         "deterministic": True,  # digests equal after the first / last timed launch and the e2e run
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(st_e2e.h2d_bytes),

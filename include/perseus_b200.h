@@ -115,7 +115,9 @@ typedef struct {
   int32_t walk_us;
   /* warps that walked it: 1 = a walker warp, > 1 = a cooperative CTA */
   int32_t warps;
-  int32_t pad;
+  /* walk start (microseconds of %globaltimer, low 31 bits); diagnostics:
+   * start_us - min over the batch = when the walk began in the launch */
+  int32_t start_us;
 } pb_frontier_summary;
 
 /* Per-point scalars; point 0 is the T* seed, point k>0 follows step k. */

@@ -102,7 +102,7 @@ class FrontierSummary(C.Structure):
         ("n_table_misses", C.c_int32),
         ("walk_us", C.c_int32),
         ("warps", C.c_int32),
-        ("pad", C.c_int32),
+        ("start_us", C.c_int32),
     ]
 
 

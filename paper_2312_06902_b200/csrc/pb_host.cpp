@@ -126,6 +126,8 @@ namespace {
 
 // Validation mirrors the reference's throws; derived arrays are the static
 // device layout (level-major computations, row records, incidence).
+pb_status derive_start(HostInst& h);
+
 pb_status validate_and_derive(HostInst& h) {
   const int32_t n = h.n, ne = static_cast<int32_t>(h.edge_tail.size());
   const int32_t nc = static_cast<int32_t>(h.cls_const.size());
@@ -277,6 +279,14 @@ pb_status validate_and_derive(HostInst& h) {
     for (int32_t j = 0; j < ne; ++j) h.net.epos[n + j] = ep[j];
     h.dep_orig = std::move(ord);
   }
+  return derive_start(h);
+}
+
+// The start-schedule-dependent part of validate_and_derive: the start in
+// internal order and the sizing estimates (T_min, T*, steps, work).
+pb_status derive_start(HostInst& h) {
+  const int32_t n = h.n, ne = static_cast<int32_t>(h.edge_tail.size());
+  h.istart.clear();
   if (!h.start.empty()) {
     h.istart.assign(n, 0);
     for (int32_t i = 0; i < n; ++i) h.istart[h.inv[i]] = h.start[i];
@@ -361,7 +371,8 @@ struct DeviceRun {
   size_t cap_static = 0, cap_out = 0, cap_ws = 0, cap_insts = 0, cap_order = 0;
   long long cap_pool = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // walk launch
+  cudaEvent_t ex0 = nullptr, ex1 = nullptr;  // H2D / D2H copies
   WidePlan wide;
   int32_t smem_ctas = 0, smem_region = 0;  // > 0: every walk runs in walk_kernel_smem
   char* h_out = nullptr;  // pinned
@@ -381,6 +392,8 @@ struct DeviceRun {
     if (h_out) cudaFreeHost(h_out);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ex0) cudaEventDestroy(ex0);
+    if (ex1) cudaEventDestroy(ex1);
     if (stream) cudaStreamDestroy(stream);
     *this = DeviceRun{};
   }
@@ -407,6 +420,7 @@ struct pb_batch {
   DeviceRun run;
   pb_run_stats stats{};
   int64_t prof[pb::kPrSlots] = {};
+  HostInst derived;  // last instance derived by pb_batch_add (kept across pb_batch_clear)
   char* h_static = nullptr;  // pinned staging of the packed static blob (reused)
   size_t h_static_cap = 0;
   // E(t) = a exp(b t) + c per curve over a contiguous range [lo, lo + size),
@@ -658,16 +672,23 @@ void pack(pb_batch* b, Packed& P, std::vector<int32_t>& cap_points, double cap_s
   std::memcpy(b->h_static, b->tables.data(), b->tables.size() * sizeof(double));
   // fill pass: instances copied in parallel straight into pinned memory
   {
-    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16u));
-    std::vector<std::thread> pool_t;
-    for (unsigned t = 0; t < nt; ++t)
-      pool_t.emplace_back([&, t] {
-        for (size_t k = t; k < N; k += nt)
-          instance_sections(b, k, true, [&](int slot, const void* p, size_t bytes) {
-            if (bytes) std::memcpy(b->h_static + P.offs[k][slot], p, bytes);
-          });
-      });
-    for (auto& th : pool_t) th.join();
+    // threads only for batches worth it (a single instance -- the drop-in's
+    // per-call path -- is copied inline: thread start-up would dominate)
+    const unsigned nt = std::max(1u, std::min<unsigned>({std::thread::hardware_concurrency(), 16u,
+                                                          static_cast<unsigned>((N + 15) / 16)}));
+    auto fill = [&](unsigned t) {
+      for (size_t k = t; k < N; k += nt)
+        instance_sections(b, k, true, [&](int slot, const void* p, size_t bytes) {
+          if (bytes) std::memcpy(b->h_static + P.offs[k][slot], p, bytes);
+        });
+    };
+    if (nt == 1) {
+      fill(0);
+    } else {
+      std::vector<std::thread> pool_t;
+      for (unsigned t = 0; t < nt; ++t) pool_t.emplace_back(fill, t);
+      for (auto& th : pool_t) th.join();
+    }
   }
   for (size_t k = 0; k < N; ++k) {
     const HostInst& h = b->insts[k];
@@ -834,6 +855,8 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
     ck(cudaStreamCreateWithFlags(&R.stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&R.ev0), "event");
     ck(cudaEventCreate(&R.ev1), "event");
+    ck(cudaEventCreate(&R.ex0), "event");
+    ck(cudaEventCreate(&R.ex1), "event");
     ck(cudaMalloc(&R.d_counter, 3 * sizeof(int32_t)), "malloc counter");
     ck(cudaMalloc(&R.d_counters, sizeof(pb::RunCounters)), "malloc counters");
     ck(cudaMalloc(&R.d_pool_cursor, sizeof(unsigned long long)), "malloc cursor");
@@ -842,9 +865,7 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   std::vector<int32_t> capp;
   pack(b, P, capp, cap_scale);
   const size_t tables_off = 0;  // tables are the first section of the blob
-  cudaEvent_t h0, h1;
-  ck(cudaEventCreate(&h0), "event");
-  ck(cudaEventCreate(&h1), "event");
+  cudaEvent_t h0 = R.ex0, h1 = R.ex1;
   ensure_device(R.d_static, R.cap_static, P.stat_bytes, "malloc static");
   R.out_bytes = std::max<size_t>(P.out_bytes, 256);
   if (R.cap_out < R.out_bytes) {
@@ -917,8 +938,6 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   ck(cudaStreamSynchronize(R.stream), "sync");
   float ms = 0;
   cudaEventElapsedTime(&ms, h0, h1);
-  cudaEventDestroy(h0);
-  cudaEventDestroy(h1);
   b->stats = pb_run_stats{};
   b->stats.h2d_ms = ms;
   b->stats.h2d_bytes = static_cast<int64_t>(P.stat_bytes + sizeof(pb::DevInst) * N + sizeof(int32_t) * N);
@@ -995,9 +1014,7 @@ pb_status fetch_impl(pb_batch* b) {
     return PB_OK;
   }
   ck(cudaSetDevice(R.device), "cudaSetDevice");
-  cudaEvent_t e0, e1;
-  ck(cudaEventCreate(&e0), "event");
-  ck(cudaEventCreate(&e1), "event");
+  cudaEvent_t e0 = R.ex0, e1 = R.ex1;
   ck(cudaEventRecord(e0, R.stream), "record");
   ck(cudaMemcpyAsync(R.h_out, R.d_out, R.out_bytes, cudaMemcpyDeviceToHost, R.stream), "D2H out");
   unsigned long long used = 0;
@@ -1017,8 +1034,6 @@ pb_status fetch_impl(pb_batch* b) {
   ck(cudaStreamSynchronize(R.stream), "sync");
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   b->outp = R.h_out;  // results stay in the pinned buffer until the next run
   b->stats.d2h_ms = ms;
   b->stats.d2h_bytes = static_cast<int64_t>(R.out_bytes + 5 * nused + sizeof used);
@@ -1198,11 +1213,34 @@ pb_status pb_batch_add(pb_batch* b, const pb_instance_desc* d, int32_t* out_inde
   h.watts = d->blocking_watts;
   h.quantum = d->quantum_us;
   h.tau = d->tau;
-  if (d->start_planned_t) h.start.assign(d->start_planned_t, d->start_planned_t + d->n);
   h.max_steps = d->max_steps;
-  const pb_status s = validate_and_derive(h);
-  if (s != PB_OK) return s;
-  b->insts.push_back(std::move(h));
+  // Same DAG and cost model as the handle's last derived instance (a
+  // get_next_schedule chain through the drop-in): reuse its derived layout,
+  // redo only the start-dependent part
+  const HostInst& c = b->derived;
+  if (c.n == h.n && c.n > 0 && c.tau == h.tau && c.quantum == h.quantum && c.watts == h.watts &&
+      c.comp_class == h.comp_class && c.edge_tail == h.edge_tail && c.edge_head == h.edge_head &&
+      c.cls_const == h.cls_const && c.cls_pt_off == h.cls_pt_off && c.pt_freq == h.pt_freq &&
+      c.pt_time == h.pt_time && c.pt_energy == h.pt_energy && c.cls_trange == h.cls_trange &&
+      std::memcmp(c.cls_curve.data(), h.cls_curve.data(), sizeof(double) * h.cls_curve.size()) == 0) {
+    HostInst r = c;
+    if (d->start_planned_t) r.start.assign(d->start_planned_t, d->start_planned_t + d->n);
+    r.max_steps = d->max_steps;
+    if (!r.start.empty())
+      for (int64_t t : r.start)
+        if (t < 0) return fail(PB_ERR_INVALID_ARGUMENT, "durations must be non-negative");
+    const pb_status s = derive_start(r);
+    if (s != PB_OK) return s;
+    b->insts.push_back(std::move(r));
+  } else {
+    if (d->start_planned_t) h.start.assign(d->start_planned_t, d->start_planned_t + d->n);
+    const pb_status s = validate_and_derive(h);
+    if (s != PB_OK) return s;
+    b->derived = h;
+    b->derived.start.clear();
+    b->derived.istart.clear();
+    b->insts.push_back(std::move(h));
+  }
   b->have_results = false;
   if (out_index) *out_index = static_cast<int32_t>(b->insts.size()) - 1;
   return PB_OK;

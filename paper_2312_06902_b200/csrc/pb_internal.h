@@ -170,6 +170,7 @@ struct WsLayout {
   int64_t off_pathlog;                 // int32 [V] log entry of each path arc (BFS restart)
   int64_t off_lvlstart;                // int32 [V + 2] first log index of each BFS level
   int64_t off_nodeli;                  // int32 [V] log index of each node in the last BFS
+  int64_t off_par;                     // int32 [V] parent log index of each log entry
   int64_t stride;
   int32_t smem_bytes;  // dynamic shared memory per warp
   int32_t wide_par = 0;  // cooperative kernel: shared parent links for max_v log entries (0: none)
@@ -215,6 +216,7 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   L.off_pathlog = take(4 * max_v);
   L.off_lvlstart = take(4 * (max_v + 2));
   L.off_nodeli = take(4 * max_v);
+  L.off_par = take(4 * max_v);
   L.stride = o;
   const int64_t bitwords = (max_v + 31) / 32;
   // frontier, visited bitset, partner-ok bitset, sweep rings (fwd, bwd)
@@ -312,7 +314,7 @@ int launch_walks_smem(const DevInst* d_insts, int32_t n_inst, const int32_t* d_o
 // Bytes a walk needs to be fully shared-memory resident (bind_smem's arrays,
 // 16 B aligned each).
 inline int64_t smem_footprint(int64_t n, int64_t V, int64_t E, int64_t ne, int64_t levels, int64_t nsnk) {
-  const int64_t a[] = {16 * E, 32 * E, 4 * (V + 1), 16 * V, 4 * V, 4 * (V + 2), 4 * (levels + 1), 8 * n, 16 * n,
+  const int64_t a[] = {16 * E, 32 * E, 4 * (V + 1), 16 * V, 4 * V, 4 * V, 4 * (V + 2), 4 * (levels + 1), 8 * n, 16 * n,
                        16 * n, 16 * n, 16 * n, 8 * n, E, n, 32 * n, 16 * n, 8 * ne, 8 * E, 8 * V, n, 4 * n,
                        4 * nsnk, 4 * n};
   int64_t t = 0;

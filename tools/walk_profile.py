@@ -53,6 +53,7 @@ def profile(name):
     print(f"   arc_scans/step {st.arc_scans / S:.0f}, node_updates/step {st.node_updates / S:.0f}; "
           f"smem walks {st.smem_walks} (region {st.smem_region} B), cooperative walks {st.wide_walks}")
     walks = sorted(((b.summary(k).walk_us, k) for k in range(len(b))), reverse=True)
+    t0 = min(b.summary(k).start_us for k in range(len(b)))
     if len(walks) > 1:
         import heapq
         slots = [0.0] * min(len(walks), int(os.environ.get("PB_SLOTS", "1776")))
@@ -62,8 +63,23 @@ def profile(name):
             heapq.heappush(slots, t + us)
         print(f"   walks: longest {walks[0][0] / 1e3:.1f} ms, median {walks[len(walks) // 2][0] / 1e3:.2f} ms, "
               f"sum {sum(w for w, _ in walks) / 1e6:.1f} s; LPT replay makespan {max(slots) / 1e3:.1f} ms")
+        ends = sorted(((b.summary(k).start_us - t0 + b.summary(k).walk_us, k) for k in range(len(b))), reverse=True)
+        print("   last to finish (end ms, start ms, walk ms, index, steps, warps): " + ", ".join(
+            f"{e / 1e3:.0f}/{(b.summary(k).start_us - t0) / 1e3:.0f}/{b.summary(k).walk_us / 1e3:.0f}/{k}/"
+            f"{b.summary(k).steps}/{b.summary(k).warps}" for e, k in ends[:8]))
         print("   top walks (ms, index, steps): " + ", ".join(
             f"{us / 1e3:.0f}/{k}/{b.summary(k).steps}" for us, k in walks[:8]))
+    if os.environ.get("PB_PROFILE_DUMP"):  # per-walk table for work-model fits
+        import json as _j
+        with open(os.environ["PB_PROFILE_DUMP"], "w") as f:
+            for k in range(len(b)):
+                sm = b.summary(k)
+                pp = None
+                if name.startswith("batch:"):
+                    q = g9.batch_params(k)
+                    pp = [q.stages, q.microbatches]
+                f.write(_j.dumps({"k": k, "steps": sm.steps, "walk_us": sm.walk_us, "start_us": sm.start_us - t0,
+                                  "warps": sm.warps, "n": b._packed[k].n, "shape": pp}) + "\n")
     if bad:
         print("   FAILED (index, status, detail, steps):", bad[:10])
 
