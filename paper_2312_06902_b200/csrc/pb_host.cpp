@@ -128,6 +128,26 @@ namespace {
 // device layout (level-major computations, row records, incidence).
 pb_status derive_start(HostInst& h);
 
+// Estimated device time of a walk (ns), for the LPT order, the cooperative
+// head and the device split only (never for results).  A step's cost is
+// latency-bound and grows with the DAG's width (BFS levels and the sweep's
+// levels carry ~width arcs / computations, several rounds each) and its size
+// (the capacity pass scans every edge): per step ~ 79 ns x width + 0.0223 ns
+// x E - 226 ns (us units in the fit; least squares over the 4096 config-5
+// walks on one B200, Spearman 0.976 vs 0.958 for E x steps).  PB_WORK_MODEL=0
+// restores E x steps.
+int64_t walk_work(const HostInst& h) {
+  const int64_t E = h.n + static_cast<int64_t>(h.edge_tail.size()) + 1;
+  static const bool edges_only = [] {
+    const char* e = std::getenv("PB_WORK_MODEL");
+    return e && std::atoi(e) == 0;
+  }();
+  if (edges_only) return E * h.est_steps;
+  const double width = static_cast<double>(h.n) / std::max(1, h.n_levels);
+  const double per_step = std::max(10.0, 79.0 * width + 0.0223 * static_cast<double>(E) - 226.0);
+  return static_cast<int64_t>(per_step * 1000.0) * h.est_steps;
+}
+
 pb_status validate_and_derive(HostInst& h) {
   const int32_t n = h.n, ne = static_cast<int32_t>(h.edge_tail.size());
   const int32_t nc = static_cast<int32_t>(h.cls_const.size());
@@ -285,7 +305,7 @@ pb_status validate_and_derive(HostInst& h) {
 // The start-schedule-dependent part of validate_and_derive: the start in
 // internal order and the sizing estimates (T_min, T*, steps, work).
 pb_status derive_start(HostInst& h) {
-  const int32_t n = h.n, ne = static_cast<int32_t>(h.edge_tail.size());
+  const int32_t n = h.n;
   h.istart.clear();
   if (!h.start.empty()) {
     h.istart.assign(n, 0);
@@ -307,7 +327,7 @@ pb_status derive_start(HostInst& h) {
     h.est_steps = gap / h.tau + 2;
     if (h.max_steps > 0) h.est_steps = std::min<int64_t>(h.est_steps, h.max_steps);
   }
-  h.work = static_cast<int64_t>(n + ne + 1) * h.est_steps;
+  h.work = walk_work(h);
   return PB_OK;
 }
 
@@ -787,10 +807,12 @@ WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int s
   int n = env_int("PB_WIDE", -1);
   if (n < 0) {
     n = 0;
-    // measured on the 4096 batch: the walks with >= 75% of the largest
-    // estimated work on 2-warp CTAs, all concurrently (up to 128), give the
-    // shortest batch (10.1 s vs 10.9 s at 88% / 48 CTAs)
-    const int permille = env_int("PB_WIDE_PERMILLE", 750);
+    // measured on the 4096 batch: with the width-aware work
+    // model, the walks with >= 82.5% of the largest estimated time on 2-warp
+    // CTAs (89 walks), all concurrently, give the shortest batch: 9.0-9.1 s
+    // vs 9.4 s (80%), 9.25 s (85%), 9.5 s (90%), 11.3 s (75%: more head walks
+    // than CTAs queue behind each other)
+    const int permille = env_int("PB_WIDE_PERMILLE", 825);
     if (permille > 0 && N > int64_t{sms} * per_sm) {
       const double top = static_cast<double>(b->insts[order[0]].work);
       while (n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;
@@ -1351,6 +1373,9 @@ pb_status pb_batch_run_multi(pb_batch* b, int32_t n_devices, const int32_t* devi
       b->stats.rounds += s.stats.rounds;
       b->stats.comp_visits += s.stats.comp_visits;
       b->stats.kernel_launches += s.stats.kernel_launches;
+      b->stats.smem_walks += s.stats.smem_walks;
+      b->stats.wide_walks += s.stats.wide_walks;
+      b->stats.smem_region = std::max(b->stats.smem_region, s.stats.smem_region);
     }
     b->out = std::move(out);
     b->outp = b->out.data();
@@ -2249,7 +2274,7 @@ pb_status pb_batch_set_max_steps(pb_batch* b, int32_t max_steps) {
     } else {
       h.est_steps = std::max<int64_t>(1, max_steps);
     }
-    h.work = static_cast<int64_t>(h.n + static_cast<int64_t>(h.edge_tail.size()) + 1) * h.est_steps;
+    h.work = walk_work(h);
   }
   b->have_results = false;
   return PB_OK;

@@ -30,6 +30,10 @@ def profile(name):
     elif name.startswith("inst:"):  # single config-5 instances: inst:3284[,1580...]
         for i in name.split(":")[1].split(","):
             b.add_g9(g9.batch_params(int(i)))
+    elif name.startswith("shard:"):  # shard:R:W = rank R's LPT shard of the 4096 batch over W GPUs
+        from paper_2312_06902_b200 import shard
+        _, r, w = name.split(":")
+        b.add_g9_indices(shard.lpt_shard([shard.g9_work_estimate(i) for i in range(4096)], int(w))[int(r)])
     elif name.startswith("batch:"):
         for i in range(int(name.split(":")[1])):
             b.add_g9(g9.batch_params(i))
