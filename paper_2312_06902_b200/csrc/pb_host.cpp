@@ -818,8 +818,11 @@ WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int s
       while (n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;
     }
   }
-  w.n = static_cast<int32_t>(std::min<int64_t>(n, N));
   const int ctas = env_int("PB_WIDE_CTAS", 128);
+  // the head is at most one wave of cooperative CTAs (a batch of equal walks
+  // would otherwise queue every walk behind them)
+  if (env_int("PB_WIDE", -1) < 0) n = std::min(n, ctas);
+  w.n = static_cast<int32_t>(std::min<int64_t>(n, N));
   w.ctas = w.n > 0 ? std::max(1, std::min(ctas, w.n)) : 0;
   return w;
 }

@@ -127,7 +127,19 @@ __device__ __forceinline__ long long now() { return clock64(); }
 // L1 prefetch of the line holding p (global); no value returned, never faults.
 // Generic form: a prefetch of a shared-memory address (the shared-memory-
 // resident walk, walk_kernel_smem) performs no operation.
+#ifndef PB_PF_BFS
+#define PB_PF_BFS 1
+#endif
+#ifndef PB_PF_SWEEP
+#define PB_PF_SWEEP 1
+#endif
 __device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void pf_bfs(const void* p) {
+  if (PB_PF_BFS) pf_l1(p);
+}
+__device__ __forceinline__ void pf_sweep(const void* p) {
+  if (PB_PF_SWEEP) pf_l1(p);
+}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -421,8 +433,8 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
           if (kCoop && !kA && e.x == N.snk) atomicMin(&N.ctl->snk_li, static_cast<unsigned long long>(li));
           const int4 ent = make_int4(e.x, e.z, e.w, li);
           // the next level reads this node's arcs: start their DRAM->L1 fill now
-          pf_l1(N.ient + e.z);
-          pf_l1(N.resid + e.z);
+          pf_bfs(N.ient + e.z);
+          pf_bfs(N.resid + e.z);
           if (pos < kFrontCap)
             sts128(fnxt + 16u * pos, ent);
           else
@@ -441,8 +453,8 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
           if (lz < N.par_cap) N.par[lz] = fe.w;
           N.node_li[z] = lz;
           const int4 ent = make_int4(z, zo, ze, lz);
-          pf_l1(N.ient + zo);
-          pf_l1(N.resid + zo);
+          pf_bfs(N.ient + zo);
+          pf_bfs(N.resid + zo);
           if (posz < kFrontCap)
             sts128(fnxt + 16u * posz, ent);
           else
@@ -975,9 +987,9 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
         if (pf < want) {
           const int r = pf + 8 * s;
           if (r < want) {
-            pf_l1(row + r);
-            pf_l1(dp + r);
-            pf_l1(dr + r);
+            pf_sweep(row + r);
+            pf_sweep(dp + r);
+            pf_sweep(dr + r);
           }
           pf = min(want, pf + 128);
         }
@@ -986,8 +998,8 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
         if (pf > want) {
           const int r = pf - 8 * (s + 1);
           if (r >= want) {
-            pf_l1(row + r);
-            pf_l1(dp + r);
+            pf_sweep(row + r);
+            pf_sweep(dp + r);
           }
           pf = max(want, pf - 128);
         }
