@@ -1122,9 +1122,10 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
     long long te[kU], he[kU], hd[kU];
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const int j = min(base + 32 * q + ln, I.ne - 1);
+      const int jr = base + 32 * q + ln, j = min(jr, I.ne - 1);
       uv[q] = I.dep_nd[j];
-      oc[q] = W.ecrit[n + j];
+      // predicated, not clamped: the owner of the last edge may rewrite it below
+      oc[q] = jr < I.ne ? W.ecrit[n + j] : 0;
     }
     // endpoint loads, branch-free (index 0 stands in for the source / sink)
 #pragma unroll
@@ -1222,12 +1223,12 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
     // branch-free, clamped loads: all 5 x kU requests are in flight together
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const int i = min(base + 32 * q + ln, n - 1);
+      const int ir = base + 32 * q + ln, i = min(ir, n - 1);
       t[q] = W.durp[i];
       fx[q] = W.fin[i].x;
       tx[q] = W.tl[i].x;
       oc[q] = W.ecrit[i];
-      dt[q] = W.dirty[i];
+      dt[q] = ir < n ? W.dirty[i] : 0;  // predicated: the owner clears it below
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {

@@ -687,3 +687,28 @@ def test_schedules_range_matches_single_schedules(walks):
     assert len(full) == s.steps + 1
     for j in (0, s.steps // 2, s.steps):
         assert full[j] == b.schedule(0, j)
+
+
+def test_cleared_handle_walks_new_instances(walks):
+    """pb_batch_clear keeps the device context but drops every instance and
+    result: a handle reused for a different DAG, then for the first DAG again
+    with a start schedule (the derived-layout cache path), walks each exactly
+    as a fresh handle does."""
+    b = pb.FrontierBatch()
+    for spec in ("config:1", "diamond", "config:1"):
+        w = walks[spec]
+        dag, model, tau = instance_from_golden(w)
+        b.clear()
+        b.add(dag, model, tau)
+        b.run(0)
+        check_walk_against(b, 0, w, model.blocking_watts, model.quantum_us, full=False, hash_points=[0, 1])
+    # get-next from the frontier's point 5 on the cleared handle
+    w = walks["config:1"]
+    dag, model, tau = instance_from_golden(w)
+    start = b.schedule(0, 5)
+    b.clear()
+    b.add(dag, model, tau, start_planned_t=start.planned_t, max_steps=1)
+    b.run(0)
+    nxt = b.schedule(0, 1)
+    assert nxt.t_planned == w["t_planned"][6]
+    assert b.step_info(0, 1).sped_up == w["sped"][5]
