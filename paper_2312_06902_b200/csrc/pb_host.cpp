@@ -805,20 +805,32 @@ WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int s
   const int64_t N = static_cast<int64_t>(order.size());
   w.warps = std::max(2, std::min(4, env_int("PB_WIDE_WARPS", 2)));
   int n = env_int("PB_WIDE", -1);
-  if (n < 0) {
+  const int ctas = env_int("PB_WIDE_CTAS", 128);
+  if (n < 0 && N > 0) {
     n = 0;
-    // measured on the 4096 batch: with the width-aware work
-    // model, the walks with >= 82.5% of the largest estimated time on 2-warp
-    // CTAs (89 walks), all concurrently, give the shortest batch: 9.0-9.1 s
-    // vs 9.4 s (80%), 9.25 s (85%), 9.5 s (90%), 11.3 s (75%: more head walks
-    // than CTAs queue behind each other)
-    const int permille = env_int("PB_WIDE_PERMILLE", 825);
-    if (permille > 0 && N > int64_t{sms} * per_sm) {
-      const double top = static_cast<double>(b->insts[order[0]].work);
-      while (n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;
+    // Walker load: the estimated walker time left after a full wave of
+    // cooperative CTAs, in units of the longest walk on all walker slots
+    // (each cooperative CTA costs its SM one 4-warp walker block).
+    const double top = static_cast<double>(b->insts[order[0]].work);
+    const int64_t head = std::min<int64_t>(ctas, N);
+    double rest = 0;
+    for (int64_t k = head; k < N; ++k) rest += static_cast<double>(b->insts[order[k]].work);
+    const double slots = std::max<double>(1.0, double(sms) * per_sm - 4.0 * std::min(head, int64_t{sms}));
+    const double load = top > 0 ? rest / (slots * top) : 0.0;
+    if (load <= 0.5) {
+      // walkers have slack (a strong-scaling shard, a small batch): a full
+      // wave of cooperative walks.  Measured on LPT shards of the 4096 batch
+      // (DESIGN.md): 1/8 shard 8.79 -> 6.52-6.73 s, 1/4 9.72 -> 7.31 s, 1/2
+      // 8.55 -> 7.83 s
+      n = static_cast<int>(head);
+    } else {
+      // walkers saturated (the 4096 batch: load 0.72): only the walks with
+      // >= 82.5% of the largest estimated time (89 walks): 9.0-9.1 s vs 9.4 s
+      // (80%), 9.25 s (85%), 9.5 s (90%)
+      const int permille = env_int("PB_WIDE_PERMILLE", 825);
+      while (permille > 0 && n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;
     }
   }
-  const int ctas = env_int("PB_WIDE_CTAS", 128);
   // the head is at most one wave of cooperative CTAs (a batch of equal walks
   // would otherwise queue every walk behind them)
   if (env_int("PB_WIDE", -1) < 0) n = std::min(n, ctas);

@@ -74,6 +74,8 @@ def test_every_golden_walk_in_one_batch(walks, monkeypatch, smem, region):
     size), the global-memory walker, and shared-memory walks whose region
     holds only part of the arrays (6000 B) or none of them."""
     monkeypatch.setenv("PB_SMEM", smem)
+    if smem == "0":
+        monkeypatch.setenv("PB_WIDE", "0")  # the global-memory walker kernel only
     if region is not None:
         monkeypatch.setenv("PB_SMEM_REGION", region)
     b = pb.FrontierBatch()
