@@ -391,9 +391,12 @@ def run_ours(args):
                        if st.smem_walks else
                        f"{st.wide_walks} longest walks on 2-warp cooperative CTAs, one warp per walk for the rest"))},
         "iterations_per_s": total_steps * args.steps / t_dev,
+        "points_per_step": int(total_points),  # frontier points of the whole batch, all ranks
         "deterministic": True,  # digests equal after the first / last timed launch and the e2e run
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(st_e2e.h2d_bytes),
-                "d2h_bytes_per_step": int(st_e2e.d2h_bytes)},
+                "d2h_bytes_per_step": int(st_e2e.d2h_bytes),
+                "breakdown_ms": {"wall": 1e3 * t_e2e / len(e2e_times), "pack": st_e2e.pack_ms,
+                                 "h2d": st_e2e.h2d_ms, "kernel": st_e2e.kernel_ms, "d2h": st_e2e.d2h_ms}},
         "gpu_launches": int(timed_launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None,

@@ -212,6 +212,7 @@ typedef struct {
   int64_t smem_walks;   /* instances walked shared-memory resident (walk_kernel_smem) */
   int64_t wide_walks;   /* instances walked by cooperative multi-warp CTAs */
   int64_t smem_region;  /* bytes of shared memory per resident walk (0: none) */
+  double pack_ms;       /* host packing of the static blob (pb_batch_prepare / run) */
 } pb_run_stats;
 pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out);
 /* Raw per-phase profile of the last launch (cycles summed over walks, then

@@ -138,6 +138,7 @@ class RunStats(C.Structure):
         ("smem_walks", C.c_int64),
         ("wide_walks", C.c_int64),
         ("smem_region", C.c_int64),
+        ("pack_ms", C.c_double),
     ]
 
 

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <array>
 #include <charconv>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -900,7 +901,9 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   }
   Packed P;
   std::vector<int32_t> capp;
+  const auto pack_t0 = std::chrono::steady_clock::now();
   pack(b, P, capp, cap_scale);
+  const double pack_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pack_t0).count();
   const size_t tables_off = 0;  // tables are the first section of the blob
   cudaEvent_t h0 = R.ex0, h1 = R.ex1;
   ensure_device(R.d_static, R.cap_static, P.stat_bytes, "malloc static");
@@ -977,6 +980,7 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   cudaEventElapsedTime(&ms, h0, h1);
   b->stats = pb_run_stats{};
   b->stats.h2d_ms = ms;
+  b->stats.pack_ms = pack_ms;
   b->stats.h2d_bytes = static_cast<int64_t>(P.stat_bytes + sizeof(pb::DevInst) * N + sizeof(int32_t) * N);
   return PB_OK;
 }
