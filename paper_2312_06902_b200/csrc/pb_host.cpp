@@ -942,7 +942,22 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
       int32_t region = 0, per = 0;
       if (pb::smem_walk_plan(R.ws, fmax, &region, &per) != 0) throw CudaError("smem walk plan");
       const int64_t cap = int64_t{sms} * per;
-      if (per > 0 && (mode == 1 || static_cast<int64_t>(N) <= cap)) {
+      // Wide DAGs that do not fit the region walk faster on the cooperative
+      // kernel (2 warps split every BFS level): measured alone, width
+      // n / levels >= 11 gains 13-19% (config 4 936 -> 757 us/step, 16x256
+      // 1,065 -> 911), width 6-8 loses 2-3x (its discovery order finds many
+      // more augmenting paths), DESIGN.md.  A batch made only of such walks,
+      // one CTA each, goes cooperative instead.
+      bool all_wide = mode != 1 && static_cast<int64_t>(N) <= std::min<int64_t>(sms, 128);
+      for (size_t k = 0; all_wide && k < N; ++k) {
+        const pb::DevInst& d = P.dev[k];
+        all_wide = static_cast<double>(d.n) >= 11.0 * std::max(1, d.n_levels) &&
+                   pb::smem_footprint(d.n, d.V, d.E, d.ne, d.n_levels, d.n_snk) > region;
+      }
+      if (all_wide) {
+        R.wide.n = static_cast<int32_t>(N);
+        R.wide.ctas = static_cast<int32_t>(N);
+      } else if (per > 0 && (mode == 1 || static_cast<int64_t>(N) <= cap)) {
         R.smem_ctas = static_cast<int32_t>(std::min<int64_t>(static_cast<int64_t>(N), cap));
         R.smem_region = region;
         R.wide = WidePlan{};

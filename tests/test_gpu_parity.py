@@ -714,3 +714,18 @@ def test_cleared_handle_walks_new_instances(walks):
     nxt = b.schedule(0, 1)
     assert nxt.t_planned == w["t_planned"][6]
     assert b.step_info(0, 1).sped_up == w["sped"][5]
+
+
+def test_config4_alone_on_the_cooperative_kernel():
+    """A lone wide DAG that does not fit a shared-memory region (config 4,
+    16x128: width n / levels = 14) is walked by a 2-warp cooperative CTA:
+    bit-exact against the reference walk, every point and schedule hash."""
+    from conftest import load_golden
+    w = next(r for r in load_golden("walks_large.jsonl.gz") if r["spec"] == "config:4")
+    dag, model, tau = instance_from_golden(w)
+    b = pb.FrontierBatch()
+    b.add(dag, model, tau)
+    b.run(0)
+    st = b.stats()
+    assert st.wide_walks == 1 and st.smem_walks == 0
+    check_walk_against(b, 0, w, model.blocking_watts, model.quantum_us, full=True)
