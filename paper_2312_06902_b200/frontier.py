@@ -11,6 +11,7 @@ per instance, a delta-encoded frontier per instance.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -280,18 +281,31 @@ class FrontierBatch:
 
 # ------------------------------------------------------------------ the API
 
+_local = threading.local()
+
+
+def _handle() -> FrontierBatch:
+    """The calling thread's persistent handle, emptied for each call (its
+    stream and device / pinned buffers are reused), as the C++ drop-in does."""
+    b = getattr(_local, "batch", None)
+    if b is None:
+        b = _local.batch = FrontierBatch()
+    b.clear()
+    return b
+
+
 def discover_frontier(dag: NodeDag, model: CostModel, tau: int = 1000) -> Frontier:
     """frontier.hpp:166-189 on the device."""
     if tau <= 0:
         raise ValueError("tau must be positive")
-    b = FrontierBatch()
+    b = _handle()
     b.add(dag, model, tau)
     b.run()
     return b.frontier(0)
 
 
 def _single(dag, model, tau, planned, max_steps):
-    b = FrontierBatch()
+    b = _handle()
     b.add(dag, model, tau, start_planned_t=planned, max_steps=max_steps)
     b.run()
     s = b.summary(0)
@@ -339,7 +353,7 @@ def discretize(schedule: EnergySchedule, dag: NodeDag, model: CostModel) -> Ener
 
 def min_energy_schedule(dag: NodeDag, model: CostModel) -> EnergySchedule:
     """frontier.hpp:73-83 (not yet discretized)."""
-    b = FrontierBatch()
+    b = _handle()
     b.add(dag, model, 1, max_steps=-1)
     b.run()
     N.raise_for_instance_status(b.summary(0).status)
