@@ -68,10 +68,6 @@ constexpr int kLaneGroupLog2 = PB_LANE_GROUP_LOG2;  // >= 0 forces lanes per fro
 constexpr unsigned kFull = 0xffffffffu;
 constexpr long long kHuge = LLONG_MAX / 4;  // return-arc capacity (never binding)
 constexpr int kMaxEnds = 32;               // phase-B path ends kept per BFS
-#ifndef PB_BFS_PIPE
-#define PB_BFS_PIPE 1
-#endif
-constexpr bool kBfsPipe = PB_BFS_PIPE;     // BFS arc loads one round ahead
 #ifndef PB_WALKER_PAR
 #define PB_WALKER_PAR 1
 #endif
@@ -339,7 +335,7 @@ __device__ int collect_ends(Net& N, int buf, int cnt) {
 // the level that marks the sink (one shared load per level) and returns the
 // number of that level's arcs into the sink, recorded in N.ends (0 = sink
 // unreachable; the bitset then marks exactly the residual-reachable set).
-template <bool kA, bool kCoop>
+template <bool kA, bool kCoop, bool kLat = false>
 __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int start) {
   const int ln = lane_id();
   const unsigned lt = lanemask_lt();
@@ -384,25 +380,18 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
       arcs += mine;
       // software pipeline: round r + 1's {ient, resid} pair is issued before
       // round r is processed (nothing in a BFS writes resid), so a node's
-      // arcs cost one dependent round trip instead of one per round
-      int4 en = make_int4(0, 0, 0, 0);  // {other, packed twin, other_off, other_end}
-      long long wn = 0;
+      // arcs cost about one dependent round trip instead of one per round.
+      // kLat (shared-memory-resident walks, 255 registers): two register
+      // buffers, so a new load never waits on the registers of the one in
+      // flight; walkers keep one (register budget, measured)
+      int4 ea = make_int4(0, 0, 0, 0), eb = ea;  // {other, packed twin, other_off, other_end}
+      long long wa = 0, wb = 0;
       if (p < fe.z) {
-        en = ldg_ient(N.ient + p);
-        wn = N.resid[p];
+        ea = ldg_ient(N.ient + p);
+        wa = N.resid[p];
       }
-      for (int r = 0; r < rounds; ++r, p += g) {
+      auto round = [&](const int4 e, const long long w, const int p) {
         const bool v = p < fe.z;
-        if (!kBfsPipe && r > 0 && v) {  // A/B reference: each round loads its own pair
-          en = ldg_ient(N.ient + p);
-          wn = N.resid[p];
-        }
-        const int4 e = en;
-        const long long w = wn;
-        if (kBfsPipe && p + g < fe.z) {
-          en = ldg_ient(N.ient + p + g);
-          wn = N.resid[p + g];
-        }
         const bool ok = v && w != 0 && w >= negS;  // e, w are stale past this lane's arcs
         const uint32_t m = ok ? 1u << (e.x & 31) : 0u;
         const uint32_t pw = lds32(N.s_pok + 4u * (e.x >> 5));  // issued beside the atomic
@@ -481,6 +470,31 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
         }
         if (!kCoop) nc += __popc(bm) + __popc(bz);
         upd += c + cz;
+      };
+      if (kLat) {
+        for (int r = 0; r < rounds; r += 2, p += 2 * g) {
+          if (p + g < fe.z) {
+            eb = ldg_ient(N.ient + p + g);
+            wb = N.resid[p + g];
+          }
+          round(ea, wa, p);
+          if (r + 1 >= rounds) break;
+          if (p + 2 * g < fe.z) {
+            ea = ldg_ient(N.ient + p + 2 * g);
+            wa = N.resid[p + 2 * g];
+          }
+          round(eb, wb, p + g);
+        }
+      } else {
+        for (int r = 0; r < rounds; ++r, p += g) {
+          const int4 e = ea;
+          const long long w = wa;
+          if (p + g < fe.z) {
+            ea = ldg_ient(N.ient + p + g);
+            wa = N.resid[p + g];
+          }
+          round(e, w, p);
+        }
       }
     }
     if (kCoop) {
@@ -545,10 +559,10 @@ __device__ void prepare_restart(Net& N, int j) {
 // BFS entry for the walk driver (warp 0): solo, or posted to the CTA's
 // helper warps (walk_kernel_wide) and run cooperatively.  start >= 0
 // restarts from that level of the last BFS (prepare_restart).
-template <bool kA>
+template <bool kA, bool kLat = false>
 __device__ int bfs(Net& N, int nsrc, int& tgt, Counters& C, int start = -1) {
   if (start >= 0) prepare_restart(N, start);
-  if (N.nw <= 1) return bfs_core<kA, false>(N, nsrc, tgt, C, 0, start);
+  if (N.nw <= 1) return bfs_core<kA, false, kLat>(N, nsrc, tgt, C, 0, start);
   if (lane_id() == 0) {
     CoopCtl* k = N.ctl;
     k->cmd = kA ? 2 : 1;
@@ -728,6 +742,7 @@ __device__ int augment_b(Net& N, int nend, Counters& C) {
 // duplicates allowed) in the circulation network (return arc enabled).
 // Returns false when some excess cannot reach any deficit: the bounded
 // network is infeasible (max_flow_lower_bounds returns nullopt).
+template <bool kLat = false>
 __device__ bool repair(Net& N, int ntouch, Counters& C) {
   const int ln = lane_id();
   if (ntouch == 0) return true;  // nothing moved: keep the last BFS state
@@ -775,7 +790,7 @@ __device__ bool repair(Net& N, int ntouch, Counters& C) {
     nex = ns;
     C.add(kPrBfsA, 1);
     int tgt;
-    const int found = bfs<true>(N, ns, tgt, C);
+    const int found = bfs<true, kLat>(N, ns, tgt, C);
     if (found < 0) {
       ok = false;
       break;
@@ -798,6 +813,7 @@ __device__ bool repair(Net& N, int ntouch, Counters& C) {
 // bitset then marks the minimal min cut's source side.
 // first_restart >= 0: the first BFS resumes the last step's final BFS from
 // that level (build_caps found no residual change below it).
+template <bool kLat = false>
 __device__ void maximize(Net& N, Counters& C, int first_restart = -1) {
   const long long t0 = now();
   int restart = N.prev_valid ? first_restart : -1;
@@ -812,7 +828,7 @@ __device__ void maximize(Net& N, Counters& C, int first_restart = -1) {
     }
     C.add(kPrBfsB, 1);
     int tgt;
-    const int nend = bfs<false>(N, 1, tgt, C, restart);
+    const int nend = bfs<false, kLat>(N, 1, tgt, C, restart);
     if (nend <= 0) break;
     restart = augment_b(N, nend, C);
   }
@@ -851,6 +867,7 @@ __device__ __forceinline__ longlong2 lds_ll2(uint32_t a) {
 // the lowest of their levels and tl above the highest (lf = 0, lb = L - 1 is
 // the full sweep).  The per-level static data (row records, level bounds) and
 // the durations are loaded one iteration ahead.
+template <bool kLat = false>
 __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr, longlong2* fin,
                       longlong2* tl, bool back, long long& msp, long long& msr, uint32_t s_ring,
                       Counters& C, int lf = 0, int lb = INT_MAX) {
@@ -981,7 +998,7 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
     }
     // each row / duration line prefetched once, ~64 computations ahead
     // (level-major order: the sweep consumes them contiguously)
-    if (k < cnt_me) {
+    if (!kLat && k < cnt_me) {  // (shared-memory walks: nothing to prefetch)
       if (fwd) {
         const int want = min(b0 + 64, I.n);
         if (pf < want) {
@@ -1395,6 +1412,7 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
   return PB_OK;
 }
 
+template <bool kLat = false>
 __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& pool, Counters& C) {
   const int ln = lane_id();
   const unsigned long long g0 = gtimer();
@@ -1422,7 +1440,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   for (int i = ln; i < n; i += 32) W.durr[i] = I.pt_time[I.cls_pt_off[I.comp_class[i]]];
   __syncwarp();
   long long t_min, unused;
-  sweep(I, W.durr, W.durr, W.fin, W.tl, false, t_min, unused, N.s_ring, C);
+  sweep<kLat>(I, W.durr, W.durr, W.fin, W.tl, false, t_min, unused, N.s_ring, C);
   for (int i = ln; i < n; i += 32) {
     const int c = I.comp_class[i];
     long long t;
@@ -1447,7 +1465,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
 
   const long long t_walk0 = now();
   long long t_cur, t_real;
-  sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_cur, t_real, N.s_ring, C);
+  sweep<kLat>(I, W.durp, W.durr, W.fin, W.tl, true, t_cur, t_real, N.s_ring, C);
   const long long t_star = t_cur;
   if (ln == 0) write_point(I, 0, t_cur, t_real, spe, spt, sre, srt, 0, 0, 0, 0, 0);
   int steps = 0;
@@ -1488,11 +1506,11 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
       break;
     }
     // ---- K4 warm-started max flow with lower bounds
-    if (!repair(N, ntouch, C)) {
+    if (!repair<kLat>(N, ntouch, C)) {
       stop = PB_STOP_INFEASIBLE;
       break;
     }
-    maximize(N, C, jprev);
+    maximize<kLat>(N, C, jprev);
     if (N.R >= N.S) {
       stop = PB_STOP_INFINITE_CUT;
       break;
@@ -1603,7 +1621,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     long long t_new;
     // computation ids are level-major: levels below imin's keep fin, above imax's keep tl
     const int lf = nd ? I.ilev[imin] : I.n_levels, lb = nd ? I.ilev[imax] : -1;
-    sweep(I, W.durp, W.durr, W.fin, W.tl, true, t_new, t_real, N.s_ring, C, lf, lb);
+    sweep<kLat>(I, W.durp, W.durr, W.fin, W.tl, true, t_new, t_real, N.s_ring, C, lf, lb);
     if (I.mode == kModeDiscover && t_new >= t_cur) {
       stop = PB_STOP_NO_PROGRESS;
       break;
@@ -1914,7 +1932,7 @@ __global__ void __launch_bounds__(32, 1) walk_kernel_smem(const DevInst* insts, 
     __syncwarp();
     WsPtrs P = G;
     bind_smem(*S, P, reg, static_cast<size_t>(region));
-    run_walk(*S, P.N, P.W, pool, C);
+    run_walk<true>(*S, P.N, P.W, pool, C);
     __syncwarp();
   }
   flush_counters(C, ctr);
