@@ -6,7 +6,10 @@
 // round trip happens per step.  Synchronization is __syncwarp only; appends
 // are ballot compactions.  The LPT head (the walks that bound the batch)
 // runs in walk_kernel_wide: 2 warps per walk, every BFS level split across
-// them (named barriers).  Per step:
+// them (named barriers).  Batches whose walks all get a CTA at once (single
+// instances: the drop-in's calls) run in walk_kernel_smem: one warp per CTA,
+// the walk's arrays placed in the CTA's shared memory as far as they fit,
+// compiled as a latency variant (run_walk<true>).  Per step:
 //
 //   K2  ONE fused longest-path sweep over the level-major computation order:
 //       lanes 0-15 run the forward pass (planned AND realized finish times,
