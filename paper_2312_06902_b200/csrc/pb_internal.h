@@ -162,7 +162,7 @@ struct WsLayout {
   int64_t off_front;                   // int4  [2V] frontier overflow (ping-pong)
   int64_t off_ecrit;                   // u8    [E] edge critical in the current network
   int64_t off_durp, off_durr;          // int64 [n]
-  int64_t off_hl;                      // int64x2 [n] {planned duration + tail, 0}
+  int64_t off_hl;                      // int64 [n] planned duration + tail
   int64_t off_fin;                     // int64x2 [n] {finish planned, finish realized}
   int64_t off_cap;                     // int64x2 [n] {lower, upper (-1 = infinite)}
   int64_t off_ccrit, off_choice;       // u8 [n] (off_ccrit: dirty flags)
@@ -204,7 +204,7 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   L.off_ecrit = take(max_e);
   L.off_durp = take(8 * max_n);
   L.off_durr = take(8 * max_n);
-  L.off_hl = take(16 * max_n);
+  L.off_hl = take(8 * max_n);
   L.off_fin = take(16 * max_n);
   L.off_cap = take(16 * max_n);
   L.off_ccrit = take(max_n);
@@ -315,7 +315,7 @@ int launch_walks_smem(const DevInst* d_insts, int32_t n_inst, const int32_t* d_o
 // 16 B aligned each).
 inline int64_t smem_footprint(int64_t n, int64_t V, int64_t E, int64_t ne, int64_t levels, int64_t nsnk) {
   const int64_t a[] = {16 * E, 32 * E, 4 * (V + 1), 16 * V, 4 * V, 4 * V, 4 * (V + 2), 4 * (levels + 1), 8 * n, 16 * n,
-                       16 * n, 16 * n, 16 * n, 8 * n, E, n, 32 * n, 16 * n, 8 * ne, 8 * E, 8 * V, n, 4 * n,
+                       16 * n, 8 * n, 16 * n, 8 * n, E, n, 32 * n, 16 * n, 8 * ne, 8 * E, 8 * V, n, 4 * n,
                        4 * nsnk, 4 * n};
   int64_t t = 0;
   for (int64_t x : a) t += align_up(x, 16);

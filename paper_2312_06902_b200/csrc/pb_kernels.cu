@@ -845,7 +845,7 @@ struct Walk {
   long long* durp;   // planned durations
   long long* durr;   // realized (discretized) durations
   longlong2* fin;    // {planned finish, realized finish}
-  longlong2* tl;     // {planned duration + longest tail to the sink, 0}
+  long long* tl;     // planned duration + longest tail to the sink
   longlong2* cap;    // {lower, upper; -1 = infinite} of critical computation edges
   uint8_t* ecrit;    // [E] edge in the current critical network
   uint8_t* dirty;    // [n] duration changed since the capacity was built
@@ -872,7 +872,7 @@ __device__ __forceinline__ longlong2 lds_ll2(uint32_t a) {
 // the durations are loaded one iteration ahead.
 template <bool kLat = false>
 __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr, longlong2* fin,
-                      longlong2* tl, bool back, long long& msp, long long& msr, uint32_t s_ring,
+                      long long* tl, bool back, long long& msp, long long& msr, uint32_t s_ring,
                       Counters& C, int lf = 0, int lb = INT_MAX) {
   const int ln = lane_id();
   const long long t0 = now();
@@ -887,7 +887,15 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
   const int4* row = fwd ? I.frow : I.brow;
   const int32_t* noff = fwd ? I.pin_off : I.pout_off;
   const int32_t* nb_ = fwd ? I.pin : I.pout;
-  longlong2* vals = fwd ? fin : tl;
+  // this half's values: {planned, realized} finish (forward) or the tail
+  // length (backward; its realized half is unused)
+  auto vload = [&](int m) -> longlong2 { return fwd ? fin[m] : make_longlong2(tl[m], 0); };
+  auto vstore = [&](int i, long long a, long long c) {
+    if (fwd)
+      fin[i] = make_longlong2(a, c);
+    else
+      tl[i] = a;
+  };
   const uint32_t ring = (fwd ? s_ring : s_ring + 16u * kRingLevels * 16);
   long long mp = 0, mr = 0;
   C.add(kPrLpLevels, iters);
@@ -900,7 +908,7 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
       if (lev < 0 || lev >= L || cnt_me <= 0) continue;
       const int b = I.lvl_off[lev], e = I.lvl_off[lev + 1];
       if (b + s < e) {
-        const longlong2 v = vals[b + s];
+        const longlong2 v = vload(b + s);
         sts_ll2(ring + 16u * ((lev % kRingLevels) * 16 + s), v.x, v.y);
       }
     }
@@ -954,28 +962,28 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
       y = max(max(v0.y, v1.y), max(v2.y, y));
       if (g0 | g1 | g2) {
         const int m = g0 ? r0.y : (g1 ? r0.z : r0.w);
-        const longlong2 v = vals[m & 0xffffff];
+        const longlong2 v = vload(m & 0xffffff);
         x = max(x, v.x);
         y = max(y, v.y);
         if (g0 && g1) {
-          const longlong2 w = vals[r0.z & 0xffffff];
+          const longlong2 w = vload(r0.z & 0xffffff);
           x = max(x, w.x);
           y = max(y, w.y);
         }
         if (g2 && (g0 || g1)) {
-          const longlong2 w = vals[r0.w & 0xffffff];
+          const longlong2 w = vload(r0.w & 0xffffff);
           x = max(x, w.x);
           y = max(y, w.y);
         }
       }
       if (cnt > 3)
         for (int j = noff[i0] + 3; j < noff[i0 + 1]; ++j) {
-          const longlong2 v = vals[nb_[j]];
+          const longlong2 v = vload(nb_[j]);
           x = max(x, v.x);
           y = max(y, v.y);
         }
       const long long a = x + dp0, c = fwd ? y + dr0 : 0;
-      vals[i0] = make_longlong2(a, c);
+      vstore(i0, a, c);
       sts_ll2(ring + 16u * ((lev_of(k) % kRingLevels) * 16 + s), a, c);
       if (fwd && (r0.x >> 16)) {
         mp = max(mp, a);
@@ -986,12 +994,12 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
       for (int i = i0 + 16; i < e0; i += 16) {
         long long xx = 0, yy = 0;
         for (int j = noff[i]; j < noff[i + 1]; ++j) {
-          const longlong2 v = vals[nb_[j]];
+          const longlong2 v = vload(nb_[j]);
           xx = max(xx, v.x);
           yy = max(yy, v.y);
         }
         const long long aa = xx + dp[i], cc = fwd ? yy + dr[i] : 0;
-        vals[i] = make_longlong2(aa, cc);
+        vstore(i, aa, cc);
         if (fwd && (row[i].x >> 16)) {
           mp = max(mp, aa);
           mr = max(mr, cc);
@@ -1246,7 +1254,7 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
       const int ir = base + 32 * q + ln, i = min(ir, n - 1);
       t[q] = W.durp[i];
       fx[q] = W.fin[i].x;
-      tx[q] = W.tl[i].x;
+      tx[q] = W.tl[i];
       oc[q] = W.ecrit[i];
       dt[q] = ir < n ? W.dirty[i] : 0;  // predicated: the owner clears it below
     }
@@ -1271,7 +1279,7 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
     if (k < nh) {
       i = W.delta[k];
       const long long t = W.durp[i];
-      const bool crit = W.fin[i].x + W.tl[i].x - t == ms;
+      const bool crit = W.fin[i].x + W.tl[i] - t == ms;
       const bool oc = W.ecrit[i];
       const CompRec rc = I.crec[i];
       long long fo = 0;
@@ -1685,7 +1693,7 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.W.durp = reinterpret_cast<long long*>(base + L.off_durp);
   p.W.durr = reinterpret_cast<long long*>(base + L.off_durr);
   p.W.fin = reinterpret_cast<longlong2*>(base + L.off_fin);
-  p.W.tl = reinterpret_cast<longlong2*>(base + L.off_hl);
+  p.W.tl = reinterpret_cast<long long*>(base + L.off_hl);
   p.W.cap = reinterpret_cast<longlong2*>(base + L.off_cap);
   p.W.ecrit = reinterpret_cast<uint8_t*>(base + L.off_ecrit);
   p.W.dirty = reinterpret_cast<uint8_t*>(base + L.off_ccrit);
@@ -1896,7 +1904,7 @@ __device__ void bind_smem(DevInst& S, WsPtrs& P, char* region, size_t cap) {
   st(S.lvl_off, 4 * (S.n_levels + 1));
   ws(P.W.durp, 8 * n);
   ws(P.W.fin, 16 * n);
-  ws(P.W.tl, 16 * n);
+  ws(P.W.tl, 8 * n);
   st(S.frow, 16 * n);
   st(S.brow, 16 * n);
   ws(P.W.durr, 8 * n);
@@ -2179,14 +2187,14 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
     for (int j = ln; j < I.ne; j += 32) {
       const int2 uv = I.dep_nd[j];
       if (uv.x == n && uv.y < n) {
-        const long long c = ms - W.tl[uv.y].x;
+        const long long c = ms - W.tl[uv.y];
         if (c < ls) ls = c;
       }
     }
     ls = wmin(ls);
     for (int i = ln; i < n; i += 32) {
       const int o = I.orig[i];
-      const long long d = W.durp[i], f = W.fin[i].x, h = W.tl[i].x;
+      const long long d = W.durp[i], f = W.fin[i].x, h = W.tl[i];
       O.earliest[2 * o] = f - d;
       O.earliest[2 * o + 1] = f;
       O.latest[2 * o + 1] = ms - (h - d);
@@ -2208,14 +2216,14 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
         tl = ls;
       } else {
         te = W.fin[uv.x].x;
-        tl = ms - (W.tl[uv.x].x - W.durp[uv.x]);
+        tl = ms - (W.tl[uv.x] - W.durp[uv.x]);
       }
       if (uv.y == n + 1) {
         he = ms;
         hl = ms;
       } else {
         he = W.fin[uv.y].x - W.durp[uv.y];
-        hl = ms - W.tl[uv.y].x;
+        hl = ms - W.tl[uv.y];
       }
       O.critical[n + I.dep_orig[j]] = te == tl && he == hl && te == he;
     }
