@@ -729,3 +729,29 @@ def test_config4_alone_on_the_cooperative_kernel():
     st = b.stats()
     assert st.wide_walks == 1 and st.smem_walks == 0
     check_walk_against(b, 0, w, model.blocking_watts, model.quantum_us, full=True)
+
+
+@pytest.mark.parametrize("shape", [(32, 512), (24, 300)])
+def test_very_large_instance_agrees_across_kernels(monkeypatch, shape):
+    """A DAG far beyond the config-5 sizes (32x512: 32,768 computations,
+    ~98k edge-centric edges; the cooperative kernel's parent links no longer
+    fit shared memory) walked for 200 steps by each kernel: the single-warp
+    walker, the cooperative CTA and the shared-memory kernel (partial
+    placement).  The minimal min cut is unique, so every point and delta
+    record must agree bit for bit (size-independent parity property)."""
+    N_, M_ = shape
+    p = g9.G9Params(N_, M_, 10, 1.1, 77, N_ // 2, 1.2)
+    digests = {}
+    for mode in ({"PB_SMEM": "0", "PB_WIDE": "0"}, {"PB_WIDE": "1"}, {"PB_SMEM": "1"}):
+        for k in ("PB_SMEM", "PB_WIDE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in mode.items():
+            monkeypatch.setenv(k, v)
+        b = pb.FrontierBatch()
+        b.add_g9(p)
+        b.set_max_steps(200)
+        b.run(0)
+        s = b.summary(0)
+        assert s.status == 0 and s.n_table_misses == 0 and s.steps == 200, (mode, s.status, s.steps)
+        digests[tuple(mode.items())] = b.digest(0)
+    assert len(set(digests.values())) == 1, digests
