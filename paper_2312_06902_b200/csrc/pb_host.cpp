@@ -1321,13 +1321,24 @@ pb_status pb_batch_run(pb_batch* b, int32_t device) {
   if (!b) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
   return guarded([&] {
     double scale = 1.0;
+    static const bool trace = std::getenv("PB_TRACE") != nullptr;
     for (int attempt = 0; attempt < 6; ++attempt) {
+      const auto t0 = std::chrono::steady_clock::now();
       pb_status s = prepare_impl(b, device, scale);
       if (s != PB_OK) return s;
+      const auto t1 = std::chrono::steady_clock::now();
       s = launch_impl(b, nullptr);
       if (s != PB_OK) return s;
+      const auto t2 = std::chrono::steady_clock::now();
       s = fetch_impl(b);
       if (s != PB_OK) return s;
+      if (trace) {
+        const auto t3 = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto z) { return std::chrono::duration<double, std::milli>(z - a).count(); };
+        std::fprintf(stderr, "pb_batch_run: %zu walks, prepare %.3f ms (pack %.3f, H2D %.3f), launch %.3f ms "
+                     "(kernel %.3f), fetch %.3f ms, attempt %d\n", b->insts.size(), ms(t0, t1), b->stats.pack_ms,
+                     b->stats.h2d_ms, ms(t1, t2), b->stats.kernel_ms, ms(t2, t3), attempt);
+      }
       if (!any_log_full(b)) return PB_OK;
       scale *= 4.0;  // rare: a walk took more steps than (T* - T_min) / tau
     }
