@@ -213,6 +213,7 @@ typedef struct {
   int64_t wide_walks;   /* instances walked by cooperative multi-warp CTAs */
   int64_t smem_region;  /* bytes of shared memory per resident walk (0: none) */
   double pack_ms;       /* host packing of the static blob (pb_batch_prepare / run) */
+  int64_t warm_starts;  /* walks that resumed the flow state of the handle's last get-next walk */
 } pb_run_stats;
 pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out);
 /* Raw per-phase profile of the last launch (cycles summed over walks, then

@@ -139,6 +139,7 @@ class RunStats(C.Structure):
         ("wide_walks", C.c_int64),
         ("smem_region", C.c_int64),
         ("pack_ms", C.c_double),
+        ("warm_starts", C.c_int64),
     ]
 
 

@@ -67,6 +67,7 @@ struct HostInst {
   pb::NetLayout net;
   std::vector<int64_t> istart;  // start schedule in internal order
   int64_t t_min_est = 0, t_star_est = 0, est_steps = 0, work = 0;
+  uint64_t gen = 0;  // pb_batch::derived_gen this instance was derived under (pb_batch_add), 0 = other
 };
 
 // Longest path on the node DAG with the given durations (internal order;
@@ -397,6 +398,8 @@ struct DeviceRun {
   WidePlan wide;
   int32_t smem_ctas = 0, smem_region = 0;  // > 0: every walk runs in walk_kernel_smem
   char* h_out = nullptr;  // pinned
+  char* d_carry = nullptr;  // warm-start state of a get-next chain (pb_internal.h CarryHdr)
+  size_t cap_carry = 0;
   void release() {
     if (device < 0) return;
     cudaSetDevice(device);
@@ -410,6 +413,7 @@ struct DeviceRun {
     cudaFree(d_pool_ids);
     cudaFree(d_pool_choice);
     cudaFree(d_pool_cursor);
+    cudaFree(d_carry);
     if (h_out) cudaFreeHost(h_out);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -442,6 +446,14 @@ struct pb_batch {
   pb_run_stats stats{};
   int64_t prof[pb::kPrSlots] = {};
   HostInst derived;  // last instance derived by pb_batch_add (kept across pb_batch_clear)
+  uint64_t derived_gen = 0;  // bumped whenever `derived` is replaced
+  // get-next chain (one instance, the drop-in's loop of get_next_schedule):
+  // the device carry buffer holds the flow state the last walk ended in,
+  // valid for the start schedule carry_start (caller order) of derived_gen
+  bool carry_valid = false;
+  uint64_t carry_gen = 0;
+  int64_t carry_tau = 0;
+  std::vector<int64_t> carry_start;
   char* h_static = nullptr;  // pinned staging of the packed static blob (reused)
   size_t h_static_cap = 0;
   // E(t) = a exp(b t) + c per curve over a contiguous range [lo, lo + size),
@@ -883,7 +895,10 @@ void ensure_device(T*& ptr, size_t& cap, size_t bytes, const char* what) {
 // the same device and are only grown.
 pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   DeviceRun& R = b->run;
-  if (R.device >= 0 && R.device != device) R.release();
+  if (R.device >= 0 && R.device != device) {
+    R.release();
+    b->carry_valid = false;
+  }
   b->have_results = false;
   const size_t N = b->insts.size();
   if (N == 0) return PB_OK;
@@ -920,6 +935,17 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
     R.cap_out = want;
   }
   bind_device(P, R.d_static, R.d_out, tables_off);
+  // get-next chain warm start: a single get-next walk of the handle's derived
+  // instance carries its flow state to the next call; it resumes when its
+  // start schedule is exactly where the last one ended
+  if (N == 1 && !b->insts[0].start.empty() && b->insts[0].max_steps >= 0 && !std::getenv("PB_NO_CARRY")) {
+    const HostInst& h = b->insts[0];
+    pb::DevInst& d = P.dev[0];
+    ensure_device(R.d_carry, R.cap_carry, pb::carry_bytes(h.n, d.E), "malloc carry");
+    d.carry = R.d_carry;
+    d.resume = b->carry_valid && h.gen != 0 && b->carry_gen == h.gen && b->carry_tau == h.tau &&
+               b->carry_start == h.start;
+  }
   R.ws = pb::make_ws_layout(P.max_n, P.max_v, P.max_e);
   {
     int sms = 0;
@@ -996,6 +1022,7 @@ pb_status prepare_impl(pb_batch* b, int32_t device, double cap_scale) {
   b->stats = pb_run_stats{};
   b->stats.h2d_ms = ms;
   b->stats.pack_ms = pack_ms;
+  b->stats.warm_starts = N == 1 && P.dev[0].resume ? 1 : 0;
   b->stats.h2d_bytes = static_cast<int64_t>(P.stat_bytes + sizeof(pb::DevInst) * N + sizeof(int32_t) * N);
   return PB_OK;
 }
@@ -1292,6 +1319,8 @@ pb_status pb_batch_add(pb_batch* b, const pb_instance_desc* d, int32_t* out_inde
     if (d->start_planned_t) h.start.assign(d->start_planned_t, d->start_planned_t + d->n);
     const pb_status s = validate_and_derive(h);
     if (s != PB_OK) return s;
+    ++b->derived_gen;
+    h.gen = b->derived_gen;
     b->derived = h;
     b->derived.start.clear();
     b->derived.istart.clear();
@@ -1317,6 +1346,33 @@ pb_status pb_batch_fetch(pb_batch* b) {
   return guarded([&] { return fetch_impl(b); });
 }
 
+namespace {
+// After a run: a single get-next walk that took its steps left its flow
+// state in the carry buffer (run_walk); remember the schedule it ended in.
+// Anything else (another instance, a zero-step walk, a stop) leaves the
+// carry as it was or invalidates it.
+void note_carry(pb_batch* b) {
+  if (b->insts.size() != 1 || b->insts[0].start.empty() || b->insts[0].max_steps < 0) {
+    if (b->insts.size() != 1 || b->insts[0].start.empty()) b->carry_valid = false;
+    return;
+  }
+  const HostInst& h = b->insts[0];
+  pb_frontier_summary s;
+  pb_batch_summary(b, 0, &s);
+  if (s.status != PB_OK || s.stop != PB_STOP_STEP_LIMIT || s.steps < 1 || !b->run.d_carry ||
+      std::getenv("PB_NO_CARRY")) {
+    b->carry_valid = false;
+    return;
+  }
+  std::vector<int64_t> pt(h.n);
+  pb_batch_schedule(b, 0, s.steps, pt.data(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  b->carry_start = std::move(pt);
+  b->carry_tau = h.tau;
+  b->carry_gen = h.gen;
+  b->carry_valid = h.gen != 0;
+}
+}  // namespace
+
 pb_status pb_batch_run(pb_batch* b, int32_t device) {
   if (!b) return fail(PB_ERR_INVALID_ARGUMENT, "null handle");
   return guarded([&] {
@@ -1339,7 +1395,10 @@ pb_status pb_batch_run(pb_batch* b, int32_t device) {
                      "(kernel %.3f), fetch %.3f ms, attempt %d\n", b->insts.size(), ms(t0, t1), b->stats.pack_ms,
                      b->stats.h2d_ms, ms(t1, t2), b->stats.kernel_ms, ms(t2, t3), attempt);
       }
-      if (!any_log_full(b)) return PB_OK;
+      if (!any_log_full(b)) {
+        note_carry(b);
+        return PB_OK;
+      }
       scale *= 4.0;  // rare: a walk took more steps than (T* - T_min) / tau
     }
     return fail(PB_ERR_LOGIC, "delta log kept overflowing");
@@ -1379,6 +1438,7 @@ pb_status pb_batch_run_multi(pb_batch* b, int32_t n_devices, const int32_t* devi
       if (st[d] != PB_OK) return fail(st[d], "device " + std::to_string(devices[d]) + ": " + msg[d]);
     // stitch results back in the original order
     b->run.release();
+    b->carry_valid = false;
     std::vector<char> out;
     b->out_points.assign(N, 0);
     b->out_summary.assign(N, 0);

@@ -121,10 +121,24 @@ struct DevInst {
   const double* tables;           // E(t) = a exp(b t) + c for t in [t_min - tab_mlo, t_max + tab_mhi]
   const double* cls_curve;        // [3 * classes] a, b, c (host expansion only)
   const int64_t* start_planned_t; // get-next mode only (internal order)
+  // Warm start of a get-next chain (pb_host.cpp prepare_impl): the flow
+  // state a single-instance get-next walk leaves in `carry` (CarryHdr +
+  // resid[2E] + cap[n] + ecrit[E] + dirty[n]); resume = 1 when this walk's
+  // start schedule is exactly the state the last one ended in.
+  char* carry;
+  int32_t resume, pad2;
   // outputs; delta records go to the batch-wide pool (DeltaPool)
   pb_point* points;             // [cap_points]
   pb_frontier_summary* summary; // [1]
 };
+
+// Header of the warm-start carry buffer (DevInst::carry), 64 B; the arrays
+// follow at 64 (resid), 64 + 16E (cap), 64 + 16E + 16n (ecrit, dirty).
+struct CarryHdr {
+  int64_t suml_lo, suml_hi, sumu_lo, sumu_hi;  // CapSums (int128 halves)
+  int64_t ninf, R, prev_step, valid;
+};
+inline size_t carry_bytes(int64_t n, int64_t E) { return 64 + 16 * E + 16 * n + E + n + 64; }
 
 // Batch-wide append-only delta log: each step reserves a contiguous range
 // with one atomicAdd, so only the used prefix is copied back.

@@ -1223,7 +1223,8 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
 // critical edge keeps its bounds and flow.  Returns PB_OK or
 // PB_ERR_OVERFLOW; ntouch = nodes whose balance moved.
 __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, bool step_changed,
-                          long long ms, CapSums& T, int& ntouch, int* extrap, Counters& C, int& jprev) {
+                          long long ms, CapSums& T, int& ntouch, int* extrap, Counters& C, int& jprev,
+                          bool all_pok = false) {
   const int ln = lane_id();
   const int n = I.n;
   // Level (in the last step's final BFS) below which no residual changes:
@@ -1408,7 +1409,7 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
   jprev = !N.prev_valid ? -1 : (jc == INT_MAX ? N.last_levels - 1 : jc);
   // shortcut bits of the rebuilt computation arcs (exact now that S is known);
   // when a carried flow may reach the sentinel, rebuild them all
-  const bool all = N.R >= N.S;
+  const bool all = N.R >= N.S || all_pok;
   const int cnt = all ? n : nh;
   for (int k = ln; k < cnt; k += 32) {
     const int i = all ? k : W.delta[k];
@@ -1439,10 +1440,19 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   N.S = 0;
   N.R = 0;
   N.prev_valid = false;
-  for (int p = ln; p < 2 * I.E; p += 32) N.resid[p] = 0;
+  // a get-next chain resumes the flow state its last call ended in
+  // (DevInst::carry): residuals, critical set, bounds, dirty flags, totals
+  const bool resume = I.resume != 0 && I.carry != nullptr;
+  const CarryHdr* ch = reinterpret_cast<const CarryHdr*>(I.carry);
+  const long long* c_resid = resume ? reinterpret_cast<const long long*>(I.carry + 64) : nullptr;
+  const longlong2* c_cap = resume ? reinterpret_cast<const longlong2*>(I.carry + 64 + 16 * I.E) : nullptr;
+  const uint8_t* c_ecrit = resume ? reinterpret_cast<const uint8_t*>(I.carry + 64 + 16 * I.E + 16 * n) : nullptr;
+  for (int p = ln; p < 2 * I.E; p += 32) N.resid[p] = resume ? c_resid[p] : 0;
   for (int v = ln; v < I.V; v += 32) N.bal[v] = 0;
-  for (int e = ln; e < I.E; e += 32) W.ecrit[e] = 0;
-  for (int i = ln; i < n; i += 32) W.dirty[i] = 0;
+  for (int e = ln; e < I.E; e += 32) W.ecrit[e] = resume ? c_ecrit[e] : 0;
+  for (int i = ln; i < n; i += 32) W.dirty[i] = resume ? c_ecrit[I.E + i] : 0;
+  if (resume)
+    for (int i = ln; i < n; i += 32) W.cap[i] = c_cap[i];
   for (int w = ln; w < N.nbitw; w += 32) sts32(N.s_pok + 4u * w, 0u);
 
   int bad = 0;
@@ -1486,6 +1496,17 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   int stop = PB_STOP_AT_TMIN;
   long long prev_step = -1;
   CapSums sums{0, 0, 0};
+  bool all_pok = false;  // rebuild every partner-ok bit in the first capacity pass
+  if (resume) {
+    sums.suml = static_cast<i128>((static_cast<unsigned __int128>(static_cast<uint64_t>(ch->suml_hi)) << 64) |
+                                  static_cast<uint64_t>(ch->suml_lo));
+    sums.sumu = static_cast<i128>((static_cast<unsigned __int128>(static_cast<uint64_t>(ch->sumu_hi)) << 64) |
+                                  static_cast<uint64_t>(ch->sumu_lo));
+    sums.ninf = ch->ninf;
+    N.R = ch->R;
+    prev_step = ch->prev_step;
+    all_pok = true;
+  }
 
   while (status == PB_OK) {
     long long step;
@@ -1511,7 +1532,8 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     const bool step_changed = step != prev_step;
     prev_step = step;
     int jprev = -1;
-    const int cs = build_caps(I, N, W, step, step_changed, t_cur, sums, ntouch, &bad, C, jprev);
+    const int cs = build_caps(I, N, W, step, step_changed, t_cur, sums, ntouch, &bad, C, jprev, all_pok);
+    all_pok = false;
     if (cs != PB_OK || __any_sync(kFull, bad != 0)) {
       status = cs != PB_OK ? cs : PB_ERR_UNSUPPORTED;
       break;
@@ -1648,6 +1670,30 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     n_ids += nd;
   }
   __syncwarp();
+  // a get-next walk that took its steps leaves its flow state for the next
+  // call of the chain (DevInst::carry)
+  if (I.carry != nullptr && I.mode == kModeGetNext && status == PB_OK && stop == PB_STOP_STEP_LIMIT && steps > 0) {
+    long long* o_resid = reinterpret_cast<long long*>(I.carry + 64);
+    longlong2* o_cap = reinterpret_cast<longlong2*>(I.carry + 64 + 16 * I.E);
+    uint8_t* o_ecrit = reinterpret_cast<uint8_t*>(I.carry + 64 + 16 * I.E + 16 * n);
+    for (int p = ln; p < 2 * I.E; p += 32) o_resid[p] = N.resid[p];
+    for (int i = ln; i < n; i += 32) o_cap[i] = W.cap[i];
+    for (int e = ln; e < I.E; e += 32) o_ecrit[e] = W.ecrit[e];
+    for (int i = ln; i < n; i += 32) o_ecrit[I.E + i] = W.dirty[i];
+    if (ln == 0) {
+      CarryHdr h;
+      h.suml_lo = static_cast<int64_t>(static_cast<uint64_t>(static_cast<unsigned __int128>(sums.suml)));
+      h.suml_hi = static_cast<int64_t>(static_cast<uint64_t>(static_cast<unsigned __int128>(sums.suml) >> 64));
+      h.sumu_lo = static_cast<int64_t>(static_cast<uint64_t>(static_cast<unsigned __int128>(sums.sumu)));
+      h.sumu_hi = static_cast<int64_t>(static_cast<uint64_t>(static_cast<unsigned __int128>(sums.sumu) >> 64));
+      h.ninf = sums.ninf;
+      h.R = N.R;
+      h.prev_step = prev_step;
+      h.valid = 1;
+      *reinterpret_cast<CarryHdr*>(I.carry) = h;
+    }
+    __syncwarp();
+  }
   const long long n_miss = wsum(bad);
   C.add(kPrWalk, now() - t_walk0);
   if (ln == 0) {

@@ -755,3 +755,39 @@ def test_very_large_instance_agrees_across_kernels(monkeypatch, shape):
         assert s.status == 0 and s.n_table_misses == 0 and s.steps == 200, (mode, s.status, s.steps)
         digests[tuple(mode.items())] = b.digest(0)
     assert len(set(digests.values())) == 1, digests
+
+
+@pytest.mark.parametrize("carry", [True, False])
+def test_get_next_chain_warm_start_matches_the_walk(walks, monkeypatch, carry):
+    """A loop of single get_next calls on one handle (the drop-in's pattern)
+    resumes each call from the flow state the previous one ended in (the
+    device carry buffer), instead of a cold max flow: every step's cut cost,
+    sped/slowed ids and planned times must equal the reference walk's, with
+    and without the warm start (PB_NO_CARRY), and the warm path must be taken."""
+    if not carry:
+        monkeypatch.setenv("PB_NO_CARRY", "1")
+    w = walks["config:2"]
+    dag, model, tau = instance_from_golden(w)
+    b = pb.FrontierBatch()
+    b.add(dag, model, tau, max_steps=-1)  # the seed (zero-step walk)
+    b.run(0)
+    planned = b.schedule(0, 0).planned_t
+    warm = 0
+    for k in range(300):
+        b.clear()
+        b.add(dag, model, tau, start_planned_t=planned, max_steps=1)
+        b.run(0)
+        warm += b.stats().warm_starts
+        s = b.summary(0)
+        assert s.status == 0 and s.steps == 1
+        info = b.step_info(0, 1)
+        assert info.cut_cost == w["cut_cost"][k], k
+        assert info.sped_up == w["sped"][k] and info.slowed_down == w["slowed"][k], k
+        nxt = b.schedule(0, 1)
+        assert nxt.t_planned == w["t_planned"][k + 1], k
+        planned = nxt.planned_t
+        if k % 50 == 7:  # a discretize (zero-step walk) in between must not break the chain
+            b.clear()
+            b.add(dag, model, tau, start_planned_t=planned, max_steps=-1)
+            b.run(0)
+    assert warm == (299 if carry else 0)
