@@ -177,7 +177,7 @@ struct WsLayout {
   int64_t off_ecrit;                   // u8    [E] edge critical in the current network
   int64_t off_durp, off_durr;          // int64 [n]
   int64_t off_hl;                      // int64 [n] planned duration + tail
-  int64_t off_fin;                     // int64x2 [n] {finish planned, finish realized}
+  int64_t off_fin;                     // int64 [n] planned finish, then int64 [max_n] realized finish
   int64_t off_cap;                     // int64x2 [n] {lower, upper (-1 = infinite)}
   int64_t off_ccrit, off_choice;       // u8 [n] (off_ccrit: dirty flags)
   int64_t off_touch, off_exl, off_delta, off_path;  // int32 lists

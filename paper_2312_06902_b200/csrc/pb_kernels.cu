@@ -844,7 +844,8 @@ __device__ void maximize(Net& N, Counters& C, int first_restart = -1) {
 struct Walk {
   long long* durp;   // planned durations
   long long* durr;   // realized (discretized) durations
-  longlong2* fin;    // {planned finish, realized finish}
+  long long* fin;    // planned finish
+  long long* finr;   // realized finish (the sweep and the realized makespan only)
   long long* tl;     // planned duration + longest tail to the sink
   longlong2* cap;    // {lower, upper; -1 = infinite} of critical computation edges
   uint8_t* ecrit;    // [E] edge in the current critical network
@@ -871,8 +872,8 @@ __device__ __forceinline__ longlong2 lds_ll2(uint32_t a) {
 // the full sweep).  The per-level static data (row records, level bounds) and
 // the durations are loaded one iteration ahead.
 template <bool kLat = false>
-__device__ void sweep(const DevInst& I, const long long* dp, const long long* dr, longlong2* fin,
-                      long long* tl, bool back, long long& msp, long long& msr, uint32_t s_ring,
+__device__ void sweep(const DevInst& I, const long long* dp, const long long* dr, long long* fin,
+                      long long* finr, long long* tl, bool back, long long& msp, long long& msr, uint32_t s_ring,
                       Counters& C, int lf = 0, int lb = INT_MAX) {
   const int ln = lane_id();
   const long long t0 = now();
@@ -889,12 +890,14 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
   const int32_t* nb_ = fwd ? I.pin : I.pout;
   // this half's values: {planned, realized} finish (forward) or the tail
   // length (backward; its realized half is unused)
-  auto vload = [&](int m) -> longlong2 { return fwd ? fin[m] : make_longlong2(tl[m], 0); };
+  auto vload = [&](int m) -> longlong2 { return fwd ? make_longlong2(fin[m], finr[m]) : make_longlong2(tl[m], 0); };
   auto vstore = [&](int i, long long a, long long c) {
-    if (fwd)
-      fin[i] = make_longlong2(a, c);
-    else
+    if (fwd) {
+      fin[i] = a;
+      finr[i] = c;
+    } else {
       tl[i] = a;
+    }
   };
   const uint32_t ring = (fwd ? s_ring : s_ring + 16u * kRingLevels * 16);
   long long mp = 0, mr = 0;
@@ -1048,9 +1051,8 @@ __device__ void sweep(const DevInst& I, const long long* dp, const long long* dr
     for (int j = ln; j < I.n_snk; j += 32) {
       const int i = I.snk[j];
       if (i >= lim) break;
-      const longlong2 v = fin[i];
-      mp = max(mp, v.x);
-      mr = max(mr, v.y);
+      mp = max(mp, fin[i]);
+      mr = max(mr, finr[i]);
     }
   }
   msp = wmax(mp);
@@ -1161,7 +1163,7 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
       const bool ts = uv[q].x == n, hs = uv[q].y == n + 1;
       const int tu = ts ? 0 : uv[q].x, hv = hs ? 0 : uv[q].y;
       const bool tcr = W.ecrit[tu], hcr = W.ecrit[hv];
-      const long long tf = W.fin[tu].x, hf = W.fin[hv].x, hdd = W.durp[hv];
+      const long long tf = W.fin[tu], hf = W.fin[hv], hdd = W.durp[hv];
       tc[q] = ts || tcr;
       hc[q] = hs || hcr;
       te[q] = ts ? 0 : tf;
@@ -1254,7 +1256,7 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
     for (int q = 0; q < kU; ++q) {
       const int ir = base + 32 * q + ln, i = min(ir, n - 1);
       t[q] = W.durp[i];
-      fx[q] = W.fin[i].x;
+      fx[q] = W.fin[i];
       tx[q] = W.tl[i];
       oc[q] = W.ecrit[i];
       dt[q] = ir < n ? W.dirty[i] : 0;  // predicated: the owner clears it below
@@ -1280,7 +1282,7 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
     if (k < nh) {
       i = W.delta[k];
       const long long t = W.durp[i];
-      const bool crit = W.fin[i].x + W.tl[i] - t == ms;
+      const bool crit = W.fin[i] + W.tl[i] - t == ms;
       const bool oc = W.ecrit[i];
       const CompRec rc = I.crec[i];
       long long fo = 0;
@@ -1461,7 +1463,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
   for (int i = ln; i < n; i += 32) W.durr[i] = I.pt_time[I.cls_pt_off[I.comp_class[i]]];
   __syncwarp();
   long long t_min, unused;
-  sweep<kLat>(I, W.durr, W.durr, W.fin, W.tl, false, t_min, unused, N.s_ring, C);
+  sweep<kLat>(I, W.durr, W.durr, W.fin, W.finr, W.tl, false, t_min, unused, N.s_ring, C);
   for (int i = ln; i < n; i += 32) {
     const int c = I.comp_class[i];
     long long t;
@@ -1486,7 +1488,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
 
   const long long t_walk0 = now();
   long long t_cur, t_real;
-  sweep<kLat>(I, W.durp, W.durr, W.fin, W.tl, true, t_cur, t_real, N.s_ring, C);
+  sweep<kLat>(I, W.durp, W.durr, W.fin, W.finr, W.tl, true, t_cur, t_real, N.s_ring, C);
   const long long t_star = t_cur;
   if (ln == 0) write_point(I, 0, t_cur, t_real, spe, spt, sre, srt, 0, 0, 0, 0, 0);
   int steps = 0;
@@ -1654,7 +1656,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     long long t_new;
     // computation ids are level-major: levels below imin's keep fin, above imax's keep tl
     const int lf = nd ? I.ilev[imin] : I.n_levels, lb = nd ? I.ilev[imax] : -1;
-    sweep<kLat>(I, W.durp, W.durr, W.fin, W.tl, true, t_new, t_real, N.s_ring, C, lf, lb);
+    sweep<kLat>(I, W.durp, W.durr, W.fin, W.finr, W.tl, true, t_new, t_real, N.s_ring, C, lf, lb);
     if (I.mode == kModeDiscover && t_new >= t_cur) {
       stop = PB_STOP_NO_PROGRESS;
       break;
@@ -1738,7 +1740,8 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.N.exl = reinterpret_cast<int32_t*>(base + L.off_exl);
   p.W.durp = reinterpret_cast<long long*>(base + L.off_durp);
   p.W.durr = reinterpret_cast<long long*>(base + L.off_durr);
-  p.W.fin = reinterpret_cast<longlong2*>(base + L.off_fin);
+  p.W.fin = reinterpret_cast<long long*>(base + L.off_fin);
+  p.W.finr = reinterpret_cast<long long*>(base + L.off_fin + 8 * L.max_n);
   p.W.tl = reinterpret_cast<long long*>(base + L.off_hl);
   p.W.cap = reinterpret_cast<longlong2*>(base + L.off_cap);
   p.W.ecrit = reinterpret_cast<uint8_t*>(base + L.off_ecrit);
@@ -1949,8 +1952,9 @@ __device__ void bind_smem(DevInst& S, WsPtrs& P, char* region, size_t cap) {
   // longest-path sweep + capacity pass
   st(S.lvl_off, 4 * (S.n_levels + 1));
   ws(P.W.durp, 8 * n);
-  ws(P.W.fin, 16 * n);
+  ws(P.W.fin, 8 * n);
   ws(P.W.tl, 8 * n);
+  ws(P.W.finr, 8 * n);
   st(S.frow, 16 * n);
   st(S.brow, 16 * n);
   ws(P.W.durr, 8 * n);
@@ -2226,7 +2230,7 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
     for (int i = ln; i < n; i += 32) W.durp[i] = O.dur[I.orig[i]];
     __syncwarp();
     long long ms, unused;
-    sweep(I, W.durp, W.durp, W.fin, W.tl, true, ms, unused, P.N.s_ring, C);
+    sweep(I, W.durp, W.durp, W.fin, W.finr, W.tl, true, ms, unused, P.N.s_ring, C);
     __syncwarp();
     // latest of the source node: min over its successors' latest start
     long long ls = ms;
@@ -2240,7 +2244,7 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
     ls = wmin(ls);
     for (int i = ln; i < n; i += 32) {
       const int o = I.orig[i];
-      const long long d = W.durp[i], f = W.fin[i].x, h = W.tl[i];
+      const long long d = W.durp[i], f = W.fin[i], h = W.tl[i];
       O.earliest[2 * o] = f - d;
       O.earliest[2 * o + 1] = f;
       O.latest[2 * o + 1] = ms - (h - d);
@@ -2261,14 +2265,14 @@ __global__ void __launch_bounds__(kBlock) slack_kernel(const DevInst* insts, con
         te = 0;
         tl = ls;
       } else {
-        te = W.fin[uv.x].x;
+        te = W.fin[uv.x];
         tl = ms - (W.tl[uv.x] - W.durp[uv.x]);
       }
       if (uv.y == n + 1) {
         he = ms;
         hl = ms;
       } else {
-        he = W.fin[uv.y].x - W.durp[uv.y];
+        he = W.fin[uv.y] - W.durp[uv.y];
         hl = ms - W.tl[uv.y];
       }
       O.critical[n + I.dep_orig[j]] = te == tl && he == hl && te == he;
