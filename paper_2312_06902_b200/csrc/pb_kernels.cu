@@ -133,6 +133,29 @@ __device__ __forceinline__ long long now() { return clock64(); }
 #define PB_PF_SWEEP 1
 #endif
 __device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.L1 [%0];" ::"l"(p)); }
+
+// Cooperative (head) walks' BFS loads carry an L2 evict-last policy
+// (createpolicy + L2::cache_hint; global memory only): their lines are the
+// last the walkers' traffic displaces.
+#ifndef PB_HEAD_EVICT_LAST
+#define PB_HEAD_EVICT_LAST 1
+#endif
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int4 ld_i4_hint(const void* a, unsigned long long pol) {
+  int4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ long long ld_s64_hint(const long long* a, unsigned long long pol) {
+  long long v;
+  asm volatile("ld.global.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ void pf_bfs(const void* p) {
   if (PB_PF_BFS) pf_l1(p);
 }
@@ -341,6 +364,7 @@ __device__ int collect_ends(Net& N, int buf, int cnt) {
 template <bool kA, bool kCoop, bool kLat = false>
 __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int start) {
   const int ln = lane_id();
+  const unsigned long long pol = kCoop && PB_HEAD_EVICT_LAST ? policy_evict_last() : 0ull;
   const unsigned lt = lanemask_lt();
   const int nw = kCoop ? N.nw : 1;
   const long long t0 = now();
@@ -390,8 +414,13 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
       int4 ea = make_int4(0, 0, 0, 0), eb = ea;  // {other, packed twin, other_off, other_end}
       long long wa = 0, wb = 0;
       if (p < fe.z) {
-        ea = ldg_ient(N.ient + p);
-        wa = N.resid[p];
+        if (kCoop && PB_HEAD_EVICT_LAST) {
+          ea = ld_i4_hint(N.ient + p, pol);
+          wa = ld_s64_hint(N.resid + p, pol);
+        } else {
+          ea = ldg_ient(N.ient + p);
+          wa = N.resid[p];
+        }
       }
       auto round = [&](const int4 e, const long long w, const int p) {
         const bool v = p < fe.z;
@@ -493,8 +522,13 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
           const int4 e = ea;
           const long long w = wa;
           if (p + g < fe.z) {
-            ea = ldg_ient(N.ient + p + g);
-            wa = N.resid[p + g];
+            if (kCoop && PB_HEAD_EVICT_LAST) {
+              ea = ld_i4_hint(N.ient + p + g, pol);
+              wa = ld_s64_hint(N.resid + p + g, pol);
+            } else {
+              ea = ldg_ient(N.ient + p + g);
+              wa = N.resid[p + g];
+            }
           }
           round(e, w, p);
         }
