@@ -364,7 +364,12 @@ __device__ int collect_ends(Net& N, int buf, int cnt) {
 template <bool kA, bool kCoop, bool kLat = false>
 __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int start) {
   const int ln = lane_id();
-  const unsigned long long pol = kCoop && PB_HEAD_EVICT_LAST ? policy_evict_last() : 0ull;
+#ifndef PB_WALKER_BFS_EL
+#define PB_WALKER_BFS_EL 0
+#endif
+  // evict-last BFS loads: cooperative walks, and (PB_WALKER_BFS_EL) global-memory walkers
+  constexpr bool kHint = PB_HEAD_EVICT_LAST && (kCoop || (PB_WALKER_BFS_EL && !kLat));
+  const unsigned long long pol = kHint ? policy_evict_last() : 0ull;
   const unsigned lt = lanemask_lt();
   const int nw = kCoop ? N.nw : 1;
   const long long t0 = now();
@@ -414,7 +419,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
       int4 ea = make_int4(0, 0, 0, 0), eb = ea;  // {other, packed twin, other_off, other_end}
       long long wa = 0, wb = 0;
       if (p < fe.z) {
-        if (kCoop && PB_HEAD_EVICT_LAST) {
+        if (kHint) {
           ea = ld_i4_hint(N.ient + p, pol);
           wa = ld_s64_hint(N.resid + p, pol);
         } else {
@@ -522,7 +527,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
           const int4 e = ea;
           const long long w = wa;
           if (p + g < fe.z) {
-            if (kCoop && PB_HEAD_EVICT_LAST) {
+            if (kHint) {
               ea = ld_i4_hint(N.ient + p + g, pol);
               wa = ld_s64_hint(N.resid + p + g, pol);
             } else {
