@@ -813,6 +813,9 @@ int env_int(const char* name, int dflt) {
 // PB_WIDE = number of instances (default: those whose estimated work is at
 // least PB_WIDE_PERMILLE of the largest, only for batches that fill the
 // device), PB_WIDE_CTAS = concurrent wide walks, PB_WIDE_WARPS = warps each.
+// DAGs whose BFS levels are wide enough for two warps to pay off.
+bool wide_dag(const HostInst& h) { return h.n >= 11 * std::max(1, h.n_levels); }
+
 WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int sms, int per_sm) {
   WidePlan w;
   const int64_t N = static_cast<int64_t>(order.size());
@@ -843,6 +846,17 @@ WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int s
       const int permille = env_int("PB_WIDE_PERMILLE", 825);
       while (permille > 0 && n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;
     }
+    // a batch of (near-)equal walks: unless every walk gets a cooperative
+    // CTA, the walker walks still take as long as before, so cooperative CTAs
+    // only cost walker slots (config 4 x 296: 4.68 s with 128 vs 4.53 s
+    // without; config 1 x 4096: 0.29 s with a cooperative head vs 0.05 s)
+    if (N > ctas && static_cast<double>(b->insts[order[N - 1]].work) * 1000.0 >= 825.0 * top) n = 0;
+    // only wide DAGs walk faster on two warps (width n / levels >= 11; on
+    // 6-8-wide DAGs the cooperative discovery order needs 2-4x the augmenting
+    // paths): the head ends at the first narrow walk
+    int wide_ok = 0;
+    while (wide_ok < n && wide_dag(b->insts[order[wide_ok]])) ++wide_ok;
+    n = wide_ok;
   }
   // the head is at most one wave of cooperative CTAs (a batch of equal walks
   // would otherwise queue every walk behind them)
