@@ -224,9 +224,13 @@ pb_status pb_batch_stats(const pb_batch* b, pb_run_stats* out);
  * paths, path arcs, steps, imbalanced nodes repaired, sweep levels. */
 pb_status pb_batch_profile(const pb_batch* b, int64_t* out, int32_t n);
 /* Drops every instance and result but keeps the handle's device context
- * (stream, device and pinned buffers) for the next add/run: a persistent
- * per-thread handle serves repeated single-instance calls (the drop-in's
- * get_next_schedule) without re-allocating. */
+ * (stream, device and pinned buffers, curve values, the last derived DAG
+ * layout) for the next add/run: a persistent per-thread handle serves
+ * repeated single-instance calls (the drop-in's get_next_schedule) without
+ * re-allocating.  A single-instance get-next run (start_planned_t set,
+ * max_steps >= 0) whose start schedule is exactly where the handle's last
+ * such run ended resumes that run's flow state on the device (warm start;
+ * results identical to a cold start, PB_NO_CARRY disables it). */
 pb_status pb_batch_clear(pb_batch* b);
 void pb_batch_destroy(pb_batch* b);
 
