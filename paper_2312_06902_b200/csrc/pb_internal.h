@@ -184,7 +184,8 @@ struct WsLayout {
   int64_t off_pathlog;                 // int32 [V] log entry of each path arc (BFS restart)
   int64_t off_lvlstart;                // int32 [V + 2] first log index of each BFS level
   int64_t off_nodeli;                  // int32 [V] log index of each node in the last BFS
-  int64_t off_par;                     // int32 [V] parent log index of each log entry
+  int64_t off_par;                     // int32 [V] parent log index of each log entry, then
+                                       // int32 [V] nearest anchor above it (path chase)
   int64_t stride;
   int32_t smem_bytes;  // dynamic shared memory per warp
   int32_t wide_par = 0;  // cooperative kernel: shared parent links for max_v log entries (0: none)
@@ -230,7 +231,7 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   L.off_pathlog = take(4 * max_v);
   L.off_lvlstart = take(4 * (max_v + 2));
   L.off_nodeli = take(4 * max_v);
-  L.off_par = take(4 * max_v);
+  L.off_par = take(8 * max_v);
   L.stride = o;
   const int64_t bitwords = (max_v + 31) / 32;
   // frontier, visited bitset, partner-ok bitset, sweep rings (fwd, bwd)

@@ -216,7 +216,17 @@ struct Net {
   int32_t* par;    // parent log index of every log entry (-1: seed): shared memory on
                    // cooperative / shared-memory-resident walks, else a compact global array
   int par_cap;     // entries par holds (0: none, chase the 16 B log entries)
+  // Path-chase anchors (global parent arrays only; off when par is in shared
+  // memory, where a hop is cheap): up[li] = par[par_cap + li] = the log index
+  // of li's ancestor at the nearest BFS level below li's that is a multiple
+  // of kAnc (-1 for a seed).  A frontier entry's .x carries what its
+  // children store.
+  bool anc;
 };
+#ifndef PB_ANCHORS
+#define PB_ANCHORS 1
+#endif
+constexpr int kAnc = 32;  // anchor level spacing (power of two)
 
 constexpr int kCtlBytes = 256;  // shared memory reserved for CoopCtl
 // Control block of a cooperative walk CTA (shared memory): warp 0 drives the
@@ -305,9 +315,10 @@ __device__ __forceinline__ bool bit_of(const Net& N, int u) {
 
 // Seeds frontier slot k (buffer 0) and log entry k with node v.
 __device__ __forceinline__ void seed(Net& N, int k, int v) {
-  fwrite(N, 0, k, make_int4(v, N.inc_off[v], N.inc_off[v + 1], k));
+  fwrite(N, 0, k, make_int4(k, N.inc_off[v], N.inc_off[v + 1], k));  // .x: children's anchor (level 0)
   N.lg[k] = make_int4(-1 - v, -1, -1, v);
   if (k < N.par_cap) N.par[k] = -1;
+  if (N.anc) N.par[N.par_cap + k] = -1;
   N.node_li[v] = k;
 }
 
@@ -401,6 +412,7 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
     int* ncp = kCoop ? &N.ctl->nc[levels % 3] : nullptr;  // reset for `levels` done by the poster
     if (kCoop && wi == 0 && ln == 0) N.ctl->nc[(levels + 1) % 3] = 0;
     ++levels;
+    const bool anc_lvl = (levels & (kAnc - 1)) == 0;  // this level's discoveries are anchors
     int nc = 0;
     for (int base = wi * (32 >> lg2); base < cnt; base += nw * (32 >> lg2)) {
       const int slot = base + (ln >> lg2);
@@ -455,9 +467,10 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
           const int li = nlog + pos;
           N.lg[li] = make_int4(p, -1, fe.w, e.x);
           if (li < N.par_cap) N.par[li] = fe.w;
+          if (N.anc) N.par[N.par_cap + li] = fe.x;
           N.node_li[e.x] = li;
           if (kCoop && !kA && e.x == N.snk) atomicMin(&N.ctl->snk_li, static_cast<unsigned long long>(li));
-          const int4 ent = make_int4(e.x, e.z, e.w, li);
+          const int4 ent = make_int4(anc_lvl ? li : fe.x, e.z, e.w, li);
           // the next level reads this node's arcs: start their DRAM->L1 fill now
           pf_bfs(N.ient + e.z);
           pf_bfs(N.resid + e.z);
@@ -477,8 +490,9 @@ __device__ int bfs_core(Net& N, int nsrc, int& tgt, Counters& C, int wi, int sta
           const int lz = nlog + posz;
           N.lg[lz] = make_int4(e.z, p, fe.w, z);  // y's computation arc, the arc into y, y's parent
           if (lz < N.par_cap) N.par[lz] = fe.w;
+          if (N.anc) N.par[N.par_cap + lz] = fe.x;
           N.node_li[z] = lz;
-          const int4 ent = make_int4(z, zo, ze, lz);
+          const int4 ent = make_int4(anc_lvl ? lz : fe.x, zo, ze, lz);
           pf_bfs(N.ient + zo);
           pf_bfs(N.resid + zo);
           if (posz < kFrontCap)
@@ -591,9 +605,11 @@ __device__ void prepare_restart(Net& N, int j) {
     const int v = N.lg[i].w;
     atoms_and(N.s_bits + 4u * (v >> 5), ~(1u << (v & 31)));
   }
+  const bool alvl = (j & (kAnc - 1)) == 0;
   for (int i = b + ln; i < e; i += 32) {
     const int v = N.lg[i].w;
-    fwrite(N, 0, i - b, make_int4(v, N.inc_off[v], N.inc_off[v + 1], i));
+    const int a = alvl ? i : (N.anc ? N.par[N.par_cap + i] : 0);
+    fwrite(N, 0, i - b, make_int4(a, N.inc_off[v], N.inc_off[v + 1], i));
   }
   __syncwarp();
 }
@@ -653,7 +669,37 @@ __device__ long long push_chain(Net& N, int first, int idx, long long cap, bool 
     // between BFSs); the warp then reads the entries together.
     int* ent = reinterpret_cast<int*>(N.fglob + N.fstride);
     int m = 0;
-    if (ln == 0) {
+    if (N.anc) {
+      // Global parent array: lane 0 follows the anchors (one hop per kAnc
+      // levels) down to the seed; then lane j walks segment j (anchor j to
+      // anchor j + 1) through the parent links, all segments at once.  A
+      // segment between two anchors spans exactly kAnc levels, one log entry
+      // each; the first one (from idx) is shorter.  Chase order does not
+      // matter to the callers (bottleneck, update and restart level are
+      // order-free), so ent = [seed, segments 1.., segment 0].
+      int* cpt = ent + 2 * N.fstride;
+      int K = 0;
+      if (ln == 0) {
+        for (int x = idx; x >= 0; x = N.par[N.par_cap + x]) cpt[K++] = x;
+      }
+      K = __shfl_sync(kFull, K, 0);
+      __syncwarp();
+      int len0 = 0;
+      for (int j = ln; j < K - 1; j += 32) {
+        int x = cpt[j];
+        const int stop = cpt[j + 1];
+        const int o = j == 0 ? 1 + (K - 2) * kAnc : 1 + (j - 1) * kAnc;
+        int t = 0;
+        while (x != stop) {
+          ent[o + t++] = x;
+          x = N.par[x];
+        }
+        if (j == 0) len0 = t;
+      }
+      if (ln == 0) ent[0] = cpt[K - 1];
+      len0 = __shfl_sync(kFull, len0, 0);
+      m = K >= 2 ? 1 + (K - 2) * kAnc + len0 : 1;
+    } else if (ln == 0) {
       for (int x = idx; x >= 0; x = N.par[x]) ent[m++] = x;
     }
     m = __shfl_sync(kFull, m, 0);
@@ -1767,6 +1813,7 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.N.fglob = reinterpret_cast<int4*>(base + L.off_front);
   p.N.par = reinterpret_cast<int32_t*>(base + L.off_par);
   p.N.par_cap = kWalkerPar ? static_cast<int>(L.max_v) : 0;
+  p.N.anc = kWalkerPar && PB_ANCHORS;
   p.N.fstride = static_cast<int>(L.max_v);
   p.N.path = reinterpret_cast<int32_t*>(base + L.off_path);
   p.N.path_log = reinterpret_cast<int32_t*>(base + L.off_pathlog);
@@ -1882,6 +1929,7 @@ __global__ void __launch_bounds__(kBlock, PB_WIDE_MIN_BLOCKS) walk_kernel_wide(c
   if (L.wide_par > 0) {  // else the global parent array of bind_ws (or the log)
     P.N.par = reinterpret_cast<int32_t*>(g_smem + nw * per + kCtlBytes);
     P.N.par_cap = L.wide_par;
+    P.N.anc = false;
   }
   if (wi == 0) {
     for (;;) {
@@ -1985,7 +2033,11 @@ __device__ void bind_smem(DevInst& S, WsPtrs& P, char* region, size_t cap) {
   st(S.ient, 32 * E);
   st(S.inc_off, 4 * (V + 1));
   ws(P.N.lg, 16 * V);
-  ws(P.N.par, 4 * V);
+  {
+    const int32_t* par0 = P.N.par;
+    ws(P.N.par, 4 * V);
+    if (P.N.par != par0) P.N.anc = false;  // shared-memory parents: plain chase
+  }
   ws(P.N.node_li, 4 * V);
   ws(P.N.lvl_start, 4 * (V + 2));
   // longest-path sweep + capacity pass
