@@ -841,9 +841,10 @@ WidePlan choose_wide(const pb_batch* b, const std::vector<int32_t>& order, int s
       n = static_cast<int>(head);
     } else {
       // walkers saturated (the 4096 batch: load 0.72): only the walks with
-      // >= 82.5% of the largest estimated time (89 walks): 9.0-9.1 s vs 9.4 s
-      // (80%), 9.25 s (85%), 9.5 s (90%)
-      const int permille = env_int("PB_WIDE_PERMILLE", 825);
+      // >= 87.5% of the largest estimated time (54 walks).  With the anchor
+      // chase (walkers 9% faster): 8.89-9.00 s vs 9.37-9.52 (80%), 9.21-9.29
+      // (82.5%), 9.00 (85%), 9.07-9.10 (90%)
+      const int permille = env_int("PB_WIDE_PERMILLE", 875);
       while (permille > 0 && n < N && static_cast<double>(b->insts[order[n]].work) * 1000.0 >= permille * top) ++n;
     }
     // a batch of (near-)equal walks: unless every walk gets a cooperative

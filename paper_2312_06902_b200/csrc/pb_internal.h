@@ -179,6 +179,7 @@ struct WsLayout {
   int64_t off_hl;                      // int64 [n] planned duration + tail
   int64_t off_fin;                     // int64 [n] planned finish, then int64 [max_n] realized finish
   int64_t off_cap;                     // int64x2 [n] {lower, upper (-1 = infinite)}
+  int64_t off_key;                     // int64x2 [n] dependency-edge criticality keys (build_caps)
   int64_t off_ccrit, off_choice;       // u8 [n] (off_ccrit: dirty flags)
   int64_t off_touch, off_exl, off_delta, off_path;  // int32 lists
   int64_t off_pathlog;                 // int32 [V] log entry of each path arc (BFS restart)
@@ -222,6 +223,7 @@ inline WsLayout make_ws_layout(int64_t max_n, int64_t max_v, int64_t max_e) {
   L.off_hl = take(8 * max_n);
   L.off_fin = take(16 * max_n);
   L.off_cap = take(16 * max_n);
+  L.off_key = take(16 * max_n);
   L.off_ccrit = take(max_n);
   L.off_choice = take(max_n);
   L.off_touch = take(4 * 2 * max_e);
@@ -330,7 +332,7 @@ int launch_walks_smem(const DevInst* d_insts, int32_t n_inst, const int32_t* d_o
 // 16 B aligned each).
 inline int64_t smem_footprint(int64_t n, int64_t V, int64_t E, int64_t ne, int64_t levels, int64_t nsnk) {
   const int64_t a[] = {16 * E, 32 * E, 4 * (V + 1), 16 * V, 4 * V, 4 * V, 4 * (V + 2), 4 * (levels + 1), 8 * n, 16 * n,
-                       16 * n, 8 * n, 16 * n, 8 * n, E, n, 32 * n, 16 * n, 8 * ne, 8 * E, 8 * V, n, 4 * n,
+                       16 * n, 8 * n, 16 * n, 8 * n, E, n, 32 * n, 16 * n, 16 * n, 8 * ne, 8 * E, 8 * V, n, 4 * n,
                        4 * nsnk, 4 * n};
   int64_t t = 0;
   for (int64_t x : a) t += align_up(x, 16);

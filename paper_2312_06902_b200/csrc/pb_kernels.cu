@@ -934,6 +934,8 @@ struct Walk {
   long long* tl;     // planned duration + longest tail to the sink
   longlong2* cap;    // {lower, upper; -1 = infinite} of critical computation edges
   uint8_t* ecrit;    // [E] edge in the current critical network
+  longlong2* key;    // [n] {critical ? finish : -1, critical ? start : -2} (build_caps):
+                     // a dependency edge u -> v is critical iff key[u].x == key[v].y
   uint8_t* dirty;    // [n] duration changed since the capacity was built
   uint8_t* choice;
   int32_t* delta;
@@ -1211,7 +1213,10 @@ struct CapSums {
 };
 
 #ifndef PB_CAP_KU
-#define PB_CAP_KU 4  // blocks of 32 * PB_CAP_KU computations / edges per round
+#define PB_CAP_KU 4  // blocks of 32 * PB_CAP_KU computations per round
+#endif
+#ifndef PB_DEP_KU
+#define PB_DEP_KU 4  // blocks of 32 * PB_DEP_KU dependency edges per round
 #endif
 
 // Dependency edges of build_caps (always infinite, lower bound 0): only
@@ -1224,7 +1229,7 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
   const int ln = lane_id();
   const int n = I.n;
   const int nw = kCoop ? N.nw : 1;
-  constexpr int kU = PB_CAP_KU;
+  constexpr int kU = PB_DEP_KU;
   auto touch_level = [&](int node) {
     if (N.prev_valid && bit_of(N, node)) {
       const int l = level_of(N, N.node_li[node]) - 1;
@@ -1234,7 +1239,7 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
   for (int base = 32 * kU * wi; base < I.ne; base += 32 * kU * nw) {
     int2 uv[kU];
     bool oc[kU], tc[kU], hc[kU];
-    long long te[kU], he[kU], hd[kU];
+    long long tk[kU], hk[kU], hd[kU];
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
       const int jr = base + 32 * q + ln, j = min(jr, I.ne - 1);
@@ -1242,18 +1247,28 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
       // predicated, not clamped: the owner of the last edge may rewrite it below
       oc[q] = jr < I.ne ? W.ecrit[n + j] : 0;
     }
-    // endpoint loads, branch-free (index 0 stands in for the source / sink)
+    // endpoint loads, branch-free (index 0 stands in for the source / sink).
+    // kCoop: one 16 B key per endpoint (the source "finishes" at 0, the sink
+    // "starts" at the makespan); walkers: criticality flags + times (fewer
+    // registers; the key stores cost the walkers more than the gathers save)
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
       const bool ts = uv[q].x == n, hs = uv[q].y == n + 1;
       const int tu = ts ? 0 : uv[q].x, hv = hs ? 0 : uv[q].y;
-      const bool tcr = W.ecrit[tu], hcr = W.ecrit[hv];
-      const long long tf = W.fin[tu], hf = W.fin[hv], hdd = W.durp[hv];
-      tc[q] = ts || tcr;
-      hc[q] = hs || hcr;
-      te[q] = ts ? 0 : tf;
-      he[q] = hs ? ms : hf;
-      hd[q] = hs ? 0 : hdd;
+      if (kCoop) {
+        const long long kt = W.key[tu].x, kh = W.key[hv].y;
+        tk[q] = ts ? 0 : kt;
+        hk[q] = hs ? ms : kh;
+      } else {
+        // every load unconditional: all 5 x kU requests in flight together
+        const bool tcr = W.ecrit[tu], hcr = W.ecrit[hv];
+        const long long tf = W.fin[tu], hf = W.fin[hv], hdd = W.durp[hv];
+        tc[q] = ts || tcr;
+        hc[q] = hs || hcr;
+        tk[q] = ts ? 0 : tf;
+        hk[q] = hs ? ms : hf;
+        hd[q] = hs ? 0 : hdd;
+      }
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
@@ -1261,7 +1276,8 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
       bool ch = false;
       int et = 0, eh = 0;
       if (j < I.ne) {
-        const bool crit = tc[q] && hc[q] && te[q] == he[q] - hd[q];
+        // kCoop: both critical (keys >= 0) and tight
+        const bool crit = kCoop ? tk[q] == hk[q] : tc[q] && hc[q] && tk[q] == hk[q] - hd[q];
         if (crit != oc[q]) {
           const int2 ps = I.epos[n + j];
           W.ecrit[n + j] = crit;
@@ -1309,9 +1325,12 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
 // computations whose duration (dirty) or the step size changed; every other
 // critical edge keeps its bounds and flow.  Returns PB_OK or
 // PB_ERR_OVERFLOW; ntouch = nodes whose balance moved.
+// kfrom: the first computation whose planned finish or duration may have
+// changed since the last call (0 on a walk's first call): dependency keys
+// below it change only with the criticality.
 __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, bool step_changed,
                           long long ms, CapSums& T, int& ntouch, int* extrap, Counters& C, int& jprev,
-                          bool all_pok = false) {
+                          int kfrom, bool all_pok = false) {
   const int ln = lane_id();
   const int n = I.n;
   // Level (in the last step's final BFS) below which no residual changes:
@@ -1353,6 +1372,8 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
       if (i < n) {
         const bool crit = fx[q] + tx[q] - t[q] == ms;
         heavy = crit != oc[q] || (crit && (dt[q] || step_changed));
+        if (N.nw > 1 && (crit != oc[q] || (i >= kfrom && (crit || kfrom == 0))))
+          W.key[i] = make_longlong2(crit ? fx[q] : -1, crit ? fx[q] - t[q] : -2);
         if (dt[q]) W.dirty[i] = 0;
       }
       wappend(heavy, i, W.delta, nh);
@@ -1595,6 +1616,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     all_pok = true;
   }
 
+  int kfrom = 0;  // build_caps: every dependency key is written on the first step
   while (status == PB_OK) {
     long long step;
     if (I.mode == kModeDiscover) {
@@ -1619,7 +1641,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     const bool step_changed = step != prev_step;
     prev_step = step;
     int jprev = -1;
-    const int cs = build_caps(I, N, W, step, step_changed, t_cur, sums, ntouch, &bad, C, jprev, all_pok);
+    const int cs = build_caps(I, N, W, step, step_changed, t_cur, sums, ntouch, &bad, C, jprev, kfrom, all_pok);
     all_pok = false;
     if (cs != PB_OK || __any_sync(kFull, bad != 0)) {
       status = cs != PB_OK ? cs : PB_ERR_UNSUPPORTED;
@@ -1741,6 +1763,7 @@ __device__ void run_walk(const DevInst& I, Net& N, Walk& W, const DeltaPool& poo
     long long t_new;
     // computation ids are level-major: levels below imin's keep fin, above imax's keep tl
     const int lf = nd ? I.ilev[imin] : I.n_levels, lb = nd ? I.ilev[imax] : -1;
+    kfrom = nd ? imin : I.n;
     sweep<kLat>(I, W.durp, W.durr, W.fin, W.finr, W.tl, true, t_new, t_real, N.s_ring, C, lf, lb);
     if (I.mode == kModeDiscover && t_new >= t_cur) {
       stop = PB_STOP_NO_PROGRESS;
@@ -1831,6 +1854,7 @@ __device__ WsPtrs bind_ws(char* base, const WsLayout& L, char* smem) {
   p.W.tl = reinterpret_cast<long long*>(base + L.off_hl);
   p.W.cap = reinterpret_cast<longlong2*>(base + L.off_cap);
   p.W.ecrit = reinterpret_cast<uint8_t*>(base + L.off_ecrit);
+  p.W.key = reinterpret_cast<longlong2*>(base + L.off_key);
   p.W.dirty = reinterpret_cast<uint8_t*>(base + L.off_ccrit);
   p.W.choice = reinterpret_cast<uint8_t*>(base + L.off_choice);
   p.W.delta = reinterpret_cast<int32_t*>(base + L.off_delta);
@@ -2053,6 +2077,7 @@ __device__ void bind_smem(DevInst& S, WsPtrs& P, char* region, size_t cap) {
   ws(P.W.dirty, n);
   st(S.crec, 32 * n);
   ws(P.W.cap, 16 * n);
+  ws(P.W.key, 16 * n);
   st(S.dep_nd, 8 * ne);
   st(S.epos, 8 * E);
   ws(P.N.bal, 8 * V);
