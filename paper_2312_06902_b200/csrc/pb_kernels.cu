@@ -232,7 +232,8 @@ constexpr int kCtlBytes = 256;  // shared memory reserved for CoopCtl
 // Control block of a cooperative walk CTA (shared memory): warp 0 drives the
 // walk and posts each BFS as a job; helper warps join it.
 struct CoopCtl {
-  int cmd;   // 0 exit, 1 BFS phase B, 2 BFS phase A, 3 capacity-pass dependency edges
+  int cmd;   // 0 exit, 1 BFS phase B, 2 BFS phase A, 3 capacity-pass dependency edges,
+             // 4 capacity-pass criticality (crit_pass)
   int nsrc;
   int start;  // restart level (-1: fresh BFS from the seeds)
   long long S;
@@ -242,7 +243,8 @@ struct CoopCtl {
   unsigned long long snk_li; // phase B: log index of the sink's discovery, ~0 = none
   // cmd 3 (capacity pass, dependency edges): inputs and per-warp results
   long long ms;
-  int ntouch;       // shared touch-list length
+  int ntouch;       // shared touch-list length (cmd 4: heavy-list length)
+  int step, kfrom;  // cmd 4: step size changed, first computation with a new finish
   int prev_valid, last_levels;
   int part_jc[4];
   long long part_dinf[4];
@@ -1325,6 +1327,56 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
 // computations whose duration (dirty) or the step size changed; every other
 // critical edge keeps its bounds and flow.  Returns PB_OK or
 // PB_ERR_OVERFLOW; ntouch = nodes whose balance moved.
+// Stage 1 of build_caps: criticality of every computation; the heavy ones
+// (criticality changed, or critical with a new duration / step size) are
+// appended to W.delta.  kCoop: warp wi of nw takes every nw-th block and
+// appends through the CTA's shared counter (N.ctl->ntouch); the dependency
+// keys are written only for cooperative walks (dep_edges<true>).
+template <bool kCoop>
+__device__ void crit_pass(const DevInst& I, Net& N, Walk& W, long long ms, bool step_changed, int kfrom, int wi,
+                          int& nh) {
+  const int ln = lane_id();
+  const int n = I.n;
+  const int nw = kCoop ? N.nw : 1;
+  constexpr int kU = PB_CAP_KU;
+  for (int base = 32 * kU * wi; base < n; base += 32 * kU * nw) {
+    long long t[kU], fx[kU], tx[kU];
+    bool oc[kU];
+    uint8_t dt[kU];
+    // branch-free, clamped loads: all 5 x kU requests are in flight together
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int ir = base + 32 * q + ln, i = min(ir, n - 1);
+      t[q] = W.durp[i];
+      fx[q] = W.fin[i];
+      tx[q] = W.tl[i];
+      oc[q] = W.ecrit[i];
+      dt[q] = ir < n ? W.dirty[i] : 0;  // predicated: the owner clears it below
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int i = base + 32 * q + ln;
+      bool heavy = false;
+      if (i < n) {
+        const bool crit = fx[q] + tx[q] - t[q] == ms;
+        heavy = crit != oc[q] || (crit && (dt[q] || step_changed));
+        if (kCoop && (crit != oc[q] || (i >= kfrom && (crit || kfrom == 0))))
+          W.key[i] = make_longlong2(crit ? fx[q] : -1, crit ? fx[q] - t[q] : -2);
+        if (dt[q]) W.dirty[i] = 0;
+      }
+      if (kCoop) {
+        const unsigned bm = __ballot_sync(kFull, heavy);
+        int at = 0;
+        if (ln == 0 && bm) at = atomicAdd(&N.ctl->ntouch, __popc(bm));
+        at = __shfl_sync(kFull, at, 0) + __popc(bm & lanemask_lt());
+        if (heavy) W.delta[at] = i;
+      } else {
+        wappend(heavy, i, W.delta, nh);
+      }
+    }
+  }
+}
+
 // kfrom: the first computation whose planned finish or duration may have
 // changed since the last call (0 on a walk's first call): dependency keys
 // below it change only with the criticality.
@@ -1351,33 +1403,23 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
   constexpr int kU = PB_CAP_KU;
   // stage 1: criticality of every computation, heavy ones compacted into W.delta
   int nh = 0;
-  for (int base = 0; base < n; base += 32 * kU) {
-    long long t[kU], fx[kU], tx[kU];
-    bool oc[kU];
-    uint8_t dt[kU];
-    // branch-free, clamped loads: all 5 x kU requests are in flight together
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int ir = base + 32 * q + ln, i = min(ir, n - 1);
-      t[q] = W.durp[i];
-      fx[q] = W.fin[i];
-      tx[q] = W.tl[i];
-      oc[q] = W.ecrit[i];
-      dt[q] = ir < n ? W.dirty[i] : 0;  // predicated: the owner clears it below
+  if (N.nw > 1) {
+    // cooperative walk: every warp takes every nw-th block
+    if (ln == 0) {
+      CoopCtl* k = N.ctl;
+      k->cmd = 4;
+      k->ms = ms;
+      k->step = step_changed ? 1 : 0;
+      k->kfrom = kfrom;
+      k->ntouch = 0;  // heavy-list counter
     }
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int i = base + 32 * q + ln;
-      bool heavy = false;
-      if (i < n) {
-        const bool crit = fx[q] + tx[q] - t[q] == ms;
-        heavy = crit != oc[q] || (crit && (dt[q] || step_changed));
-        if (N.nw > 1 && (crit != oc[q] || (i >= kfrom && (crit || kfrom == 0))))
-          W.key[i] = make_longlong2(crit ? fx[q] : -1, crit ? fx[q] - t[q] : -2);
-        if (dt[q]) W.dirty[i] = 0;
-      }
-      wappend(heavy, i, W.delta, nh);
-    }
+    __syncwarp();
+    bar_sync(1, 32 * N.nw);  // release the helpers
+    crit_pass<true>(I, N, W, ms, step_changed, kfrom, 0, nh);
+    bar_sync(2, 32 * N.nw);  // every warp's blocks are done
+    nh = *reinterpret_cast<volatile int*>(&N.ctl->ntouch);
+  } else {
+    crit_pass<false>(I, N, W, ms, step_changed, kfrom, 0, nh);
   }
   __syncwarp();
   // stage 2: heavy computations, one per lane
@@ -1975,6 +2017,15 @@ __global__ void __launch_bounds__(kBlock, PB_WIDE_MIN_BLOCKS) walk_kernel_wide(c
       if (cmd == 0) break;
       const DevInst* I = *reinterpret_cast<const DevInst* volatile*>(&ctl->inst);
       Net& N = P.N;
+      if (cmd == 4) {
+        // capacity pass, stage 1: this warp's blocks of computations
+        int unused = 0;
+        crit_pass<true>(*I, N, P.W, *reinterpret_cast<volatile long long*>(&ctl->ms),
+                        *reinterpret_cast<volatile int*>(&ctl->step) != 0,
+                        *reinterpret_cast<volatile int*>(&ctl->kfrom), wi, unused);
+        bar_sync(2, 32 * nw);
+        continue;
+      }
       if (cmd == 3) {
         // capacity pass: this warp's blocks of dependency edges
         N.prev_valid = *reinterpret_cast<volatile int*>(&ctl->prev_valid) != 0;
