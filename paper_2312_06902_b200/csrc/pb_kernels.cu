@@ -226,6 +226,9 @@ struct Net {
 #ifndef PB_ANCHORS
 #define PB_ANCHORS 1
 #endif
+#ifndef PB_ANC_GUARD
+#define PB_ANC_GUARD 1
+#endif
 constexpr int kAnc = 32;  // anchor level spacing (power of two)
 
 constexpr int kCtlBytes = 256;  // shared memory reserved for CoopCtl
@@ -692,10 +695,12 @@ __device__ long long push_chain(Net& N, int first, int idx, long long cap, bool 
         const int stop = cpt[j + 1];
         const int o = j == 0 ? 1 + (K - 2) * kAnc : 1 + (j - 1) * kAnc;
         int t = 0;
-        while (x != stop) {
+        while (x != stop && t < kAnc) {
           ent[o + t++] = x;
           x = N.par[x];
         }
+        // a segment that does not span its levels exactly means a broken log: fail loudly
+        if (PB_ANC_GUARD && (x != stop || (j > 0 && t != kAnc))) __trap();
         if (j == 0) len0 = t;
       }
       if (ln == 0) ent[0] = cpt[K - 1];
@@ -1400,7 +1405,6 @@ __device__ int build_caps(const DevInst& I, Net& N, Walk& W, long long step, boo
   ntouch = 0;
   i128 dl = 0, du = 0;
   long long dinf = 0;
-  constexpr int kU = PB_CAP_KU;
   // stage 1: criticality of every computation, heavy ones compacted into W.delta
   int nh = 0;
   if (N.nw > 1) {
