@@ -1225,6 +1225,9 @@ struct CapSums {
 #ifndef PB_DEP_KU
 #define PB_DEP_KU 4  // blocks of 32 * PB_DEP_KU dependency edges per round
 #endif
+#ifndef PB_DEP_PIPE
+#define PB_DEP_PIPE 1
+#endif
 
 // Dependency edges of build_caps (always infinite, lower bound 0): only
 // criticality changes matter.  Warp wi of nw takes every nw-th block of
@@ -1243,6 +1246,14 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
       jc = l < jc ? l : jc;
     }
   };
+  // kPipe: the next block's endpoint ids are loaded one block ahead (static
+  // data), so a block waits on one dependent round trip (its gathers), not two
+  constexpr bool kPipe = PB_DEP_PIPE == 1 || (PB_DEP_PIPE == 2 && kCoop);
+  int2 nuv[kU];
+  if (kPipe) {
+#pragma unroll
+    for (int q = 0; q < kU; ++q) nuv[q] = I.dep_nd[min(32 * kU * wi + 32 * q + ln, I.ne - 1)];
+  }
   for (int base = 32 * kU * wi; base < I.ne; base += 32 * kU * nw) {
     int2 uv[kU];
     bool oc[kU], tc[kU], hc[kU];
@@ -1250,9 +1261,13 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
       const int jr = base + 32 * q + ln, j = min(jr, I.ne - 1);
-      uv[q] = I.dep_nd[j];
+      uv[q] = kPipe ? nuv[q] : I.dep_nd[j];
       // predicated, not clamped: the owner of the last edge may rewrite it below
       oc[q] = jr < I.ne ? W.ecrit[n + j] : 0;
+    }
+    if (kPipe && base + 32 * kU * nw < I.ne) {
+#pragma unroll
+      for (int q = 0; q < kU; ++q) nuv[q] = I.dep_nd[min(base + 32 * kU * nw + 32 * q + ln, I.ne - 1)];
     }
     // endpoint loads, branch-free (index 0 stands in for the source / sink).
     // kCoop: one 16 B key per endpoint (the source "finishes" at 0, the sink
