@@ -1228,6 +1228,9 @@ struct CapSums {
 #ifndef PB_DEP_PIPE
 #define PB_DEP_PIPE 1
 #endif
+#ifndef PB_DEP_PF_OC
+#define PB_DEP_PF_OC 1
+#endif
 
 // Dependency edges of build_caps (always infinite, lower bound 0): only
 // criticality changes matter.  Warp wi of nw takes every nw-th block of
@@ -1268,6 +1271,10 @@ __device__ void dep_edges(const DevInst& I, Net& N, Walk& W, long long ms, int w
     if (kPipe && base + 32 * kU * nw < I.ne) {
 #pragma unroll
       for (int q = 0; q < kU; ++q) nuv[q] = I.dep_nd[min(base + 32 * kU * nw + 32 * q + ln, I.ne - 1)];
+      // and the next block's criticality flags (32 * kU bytes, at most two
+      // lines) into L1, without holding registers
+      if (PB_DEP_PF_OC && ln < 2)
+        pf_l1(W.ecrit + n + min(base + 32 * kU * nw + (ln ? 32 * kU - 1 : 0), I.ne - 1));
     }
     // endpoint loads, branch-free (index 0 stands in for the source / sink).
     // kCoop: one 16 B key per endpoint (the source "finishes" at 0, the sink
